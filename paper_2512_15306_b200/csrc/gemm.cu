@@ -1,0 +1,408 @@
+// Warp-specialised persistent tcgen05 GEMM for sm_100a (north-star item 2).
+//
+//   D[m, n] = sum_k A[m, k] * B[n, k]          (f32 accumulation in TMEM)
+//
+// Operands come from HBM through TMA (128-B swizzle) into a STAGES-deep smem
+// ring; one elected thread issues tcgen05.mma (kind::f8f6f4 for E4M3/E5M2,
+// kind::f16 for BF16) into a double-buffered TMEM accumulator; four epilogue
+// warps drain TMEM with tcgen05.ld and apply the reference's rounding:
+//
+//   EPI_BF16      out = bf16( acc / (sa*sb) )              src/tensorops.cpp:47,55
+//   EPI_F32       out = acc (f32)                          src/tensorops.cpp:372-376 (CE logits)
+//   EPI_BF16_RES  out = bf16( bf16(acc/(sa*sb)) + res )    src/model.cpp:281-283 (r_out)
+//   EPI_BF16_ACC  buf = SR_bf16( buf + bf16(acc/(sa*sb)) ) src/model.cpp:455-462 (GradAccumulator)
+//   EPI_F32_ACC   buf = SR_bf16( buf + acc )               (f32 grads, e.g. d_lm_w)
+//
+// Either operand may be K-major (row-major [rows][K]) or MN-major (stored
+// [K][rows]); MN-major FP8/BF16 is legal on sm_100 (UMMA a_major/b_major), so
+// dgrad and wgrad read the forward-layout tensors directly with no transposed
+// copies.  Warp roles: 0 = TMA producer, 1 = MMA issuer, 2 = TMEM allocator,
+// 4..7 = epilogue (warp%4 selects the TMEM lane quarter).
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+
+#include <cudaTypedefs.h>
+#include <mutex>
+
+namespace qtb {
+namespace gemm {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+
+struct alignas(64) Params {
+    CUtensorMap ta;
+    CUtensorMap tb;
+    int M, N, K;
+    int num_m, num_n, num_k;
+    uint32_t idesc;
+    const float* a_scale;
+    const float* b_scale;
+    void* out;
+    int64_t ldo;
+    const uint16_t* res;
+    int64_t ldr;
+    uint64_t sr_seed, sr_stream, sr_base;
+};
+
+template <int KIND, int BN>
+struct Cfg {
+    static constexpr int ELEM = KIND == 0 ? 1 : 2;
+    static constexpr int BK = 128 / ELEM;  // K elements per pipeline stage (one 128-B swizzle row)
+    static constexpr int UK = 32 / ELEM;   // K per tcgen05.mma
+    static constexpr int A_BYTES = BM * 128;
+    static constexpr int B_BYTES = BN * 128;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+};
+
+__device__ __forceinline__ void store_bf16x32(uint16_t* dst, const float (&v)[32]) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        d[q] = make_uint4(pack_bf16x2(v[8 * q + 0], v[8 * q + 1]), pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                          pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+}
+__device__ __forceinline__ void load_bf16x32(const uint16_t* src, float (&v)[32]) {
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint4 u = s[q];
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            v[8 * q + 2 * j] = __uint_as_float(w[j] << 16);
+            v[8 * q + 2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        }
+    }
+}
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col0, float denom, const uint32_t (&r)[32]) {
+    if (row >= p.M || col0 >= p.N) return;
+    const bool vec = (col0 + 32 <= p.N) && ((p.ldo & 7) == 0);
+    float v[32];
+    if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = bf16r(__fdiv_rn(__uint_as_float(r[j]), denom));
+    }
+    if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RES) {
+        uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + (int64_t)row * p.ldo + col0;
+        if constexpr (EPI == EPI_BF16_RES) {
+            const uint16_t* rs = p.res + (int64_t)row * p.ldr + col0;
+            if (vec && (p.ldr & 7) == 0) {
+                float rv[32];
+                load_bf16x32(rs, rv);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = __fadd_rn(v[j], rv[j]);
+            } else {
+                for (int j = 0; j < 32 && col0 + j < p.N; ++j) v[j] = __fadd_rn(v[j], bfbits2f(rs[j]));
+            }
+        }
+        if (vec) {
+            store_bf16x32(out, v);
+        } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = f2bfbits(v[j]);
+        }
+    } else if constexpr (EPI == EPI_F32) {
+        float* out = reinterpret_cast<float*>(p.out) + (int64_t)row * p.ldo + col0;
+        if (vec) {
+            float4* o4 = reinterpret_cast<float4*>(out);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j) out[j] = v[j];
+        }
+    } else {  // *_ACC: GradAccumulator::accumulate fused (src/model.cpp:455-462)
+        uint16_t* buf = reinterpret_cast<uint16_t*>(p.out) + (int64_t)row * p.ldo + col0;
+        const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
+        if (vec) {
+            float b[32];
+            load_bf16x32(buf, b);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) b[j] = sr_bf16(__fadd_rn(b[j], v[j]), p.sr_seed, p.sr_stream, ctr0 + j);
+            store_bf16x32(buf, b);
+        } else {
+            for (int j = 0; j < 32 && col0 + j < p.N; ++j)
+                buf[j] = f2bfbits(sr_bf16(__fadd_rn(bfbits2f(buf[j]), v[j]), p.sr_seed, p.sr_stream, ctr0 + j));
+        }
+    }
+}
+
+template <int KIND, bool A_MN, bool B_MN, int BN, int EPI>
+__global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Params p) {
+    using C = Cfg<KIND, BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + C::STAGES * C::STAGE);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&p.ta);
+        tma_prefetch(&p.tb);
+    }
+    if (warp == 1 && lane == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int tiles = p.num_m * p.num_n;
+
+    if (warp == 0 && lane == 0) {
+        // ===== TMA producer =====
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+            for (int kb = 0; kb < p.num_k; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = base + stage * C::STAGE;
+                uint8_t* sb = sa + C::A_BYTES;
+                mbar_arrive_expect_tx(&full[stage], C::STAGE);
+                const int k0 = kb * C::BK;
+                if constexpr (!A_MN) {
+                    tma_load_2d(&p.ta, &full[stage], sa, k0, m0);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < BM * C::ELEM / 128; ++i)
+                        tma_load_2d(&p.ta, &full[stage], sa + i * C::BK * 128, m0 + i * (128 / C::ELEM), k0);
+                }
+                if constexpr (!B_MN) {
+                    tma_load_2d(&p.tb, &full[stage], sb, k0, n0);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < BN * C::ELEM / 128; ++i)
+                        tma_load_2d(&p.tb, &full[stage], sb + i * C::BK * 128, n0 + i * (128 / C::ELEM), k0);
+                }
+                if (++stage == C::STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ===== MMA issuer (single thread) =====
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            mbar_wait(&tempty[acc], aphase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem + acc * BN;
+            for (int kb = 0; kb < p.num_k; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t sa = smem_u32(base + stage * C::STAGE);
+                const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < C::BK / C::UK; ++kk) {
+                    const uint64_t ad = A_MN ? make_sdesc_sw128(sa + kk * C::UK * 128, C::BK * 128, 1024)
+                                             : make_sdesc_sw128(sa + kk * 32, 16, 1024);
+                    const uint64_t bd = B_MN ? make_sdesc_sw128(sb + kk * C::UK * 128, C::BK * 128, 1024)
+                                             : make_sdesc_sw128(sb + kk * 32, 16, 1024);
+                    if constexpr (KIND == 0)
+                        mma_f8(d_tmem, ad, bd, p.idesc, (kb | kk) != 0);
+                    else
+                        mma_bf16(d_tmem, ad, bd, p.idesc, (kb | kk) != 0);
+                }
+                tc_commit(&empty[stage]);
+                if (++stage == C::STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            tc_commit(&tfull[acc]);
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: TMEM -> registers -> rounding -> HBM =====
+        const int wq = warp - 4;
+        float denom = 1.0f;
+        if (p.a_scale && p.b_scale) denom = __fmul_rn(*p.a_scale, *p.b_scale);
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (it >> 1) & 1;
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
+            const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+            const int row = m0 + wq * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
+                tmem_ld_wait();
+                epilogue_chunk<EPI>(p, row, n0 + c * 32, denom, r);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// 2-D map over a row-major matrix [outer][inner] with the given row stride.
+int make_tmap(CUtensorMap* m, const void* ptr, int elem, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+              uint32_t box_inner, uint32_t box_outer) {
+    auto fn = encode_fn();
+    if (!fn) return 900;
+    const CUtensorMapDataType dt = elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_stride_elems * (uint64_t)elem};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    const CUresult r = fn(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : 901;
+}
+
+using KernelFn = void (*)(Params);
+
+template <int KIND, bool A_MN, bool B_MN, int BN, int EPI>
+int launch(const Params& p, int grid, cudaStream_t s) {
+    using C = Cfg<KIND, BN>;
+    auto k = gemm_kernel<KIND, A_MN, B_MN, BN, EPI>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return (int)e;
+        attr_set = true;
+    }
+    k<<<grid, 256, C::SMEM, s>>>(p);
+    return (int)cudaGetLastError();
+}
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = kNumSMs;
+    }
+    return n;
+}
+
+#define QTB_GEMM_CASE(KIND, AMN, BMN, EPI)                                                            \
+    if (kind == KIND && a_mn == AMN && b_mn == BMN && epi == EPI)                                     \
+        return bn == 256 ? launch<KIND, AMN, BMN, 256, EPI>(p, grid, s)                               \
+                         : launch<KIND, AMN, BMN, 128, EPI>(p, grid, s);
+
+int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, int grid, cudaStream_t s) {
+    // FP8 block linears: fwd (K,K), dgrad (K,MN), wgrad (MN,MN); plus (K,K) for transposed-operand callers
+    QTB_GEMM_CASE(0, false, false, EPI_BF16)
+    QTB_GEMM_CASE(0, false, false, EPI_BF16_RES)
+    QTB_GEMM_CASE(0, false, true, EPI_BF16)
+    QTB_GEMM_CASE(0, true, true, EPI_BF16)
+    QTB_GEMM_CASE(0, true, true, EPI_BF16_ACC)
+    QTB_GEMM_CASE(0, false, false, EPI_BF16_ACC)
+    // BF16: LM-head logits (K,K)->f32, CE dgrad (K,MN)->bf16, CE wgrad (MN,MN)->f32 SR-accumulate
+    QTB_GEMM_CASE(1, false, false, EPI_F32)
+    QTB_GEMM_CASE(1, false, false, EPI_BF16)
+    QTB_GEMM_CASE(1, false, true, EPI_BF16)
+    QTB_GEMM_CASE(1, false, true, EPI_F32)
+    QTB_GEMM_CASE(1, true, true, EPI_F32)
+    QTB_GEMM_CASE(1, true, true, EPI_F32_ACC)
+    QTB_GEMM_CASE(1, true, true, EPI_BF16)
+    return 902;  // unsupported combination
+}
+
+}  // namespace gemm
+}  // namespace qtb
+
+using namespace qtb;
+
+extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
+    using namespace qtb::gemm;
+    if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;
+    const int elem = g->kind == 0 ? 1 : 2;
+    const int bk = 128 / elem;
+    // TMA: 16-B aligned base and row strides, leading dims cover the extents
+    if ((reinterpret_cast<uintptr_t>(g->a) & 15) || (reinterpret_cast<uintptr_t>(g->b) & 15) ||
+        ((g->lda * elem) & 15) || ((g->ldb * elem) & 15))
+        return 1;
+    if (g->lda < (g->a_mn ? g->M : g->K) || g->ldb < (g->b_mn ? g->N : g->K)) return 1;
+    int bn = g->bn;
+    if (bn != 128 && bn != 256) bn = g->N <= 128 ? 128 : 256;
+    Params p;
+    memset(&p, 0, sizeof(p));
+    int rc;
+    // A: K-major stored [M][lda]; MN-major stored [K][lda]
+    if (!g->a_mn)
+        rc = make_tmap(&p.ta, g->a, elem, g->K, g->M, g->lda, bk, BM);
+    else
+        rc = make_tmap(&p.ta, g->a, elem, g->M, g->K, g->lda, 128 / elem, bk);
+    if (rc) return rc;
+    if (!g->b_mn)
+        rc = make_tmap(&p.tb, g->b, elem, g->K, g->N, g->ldb, bk, bn);
+    else
+        rc = make_tmap(&p.tb, g->b, elem, g->N, g->K, g->ldb, 128 / elem, bk);
+    if (rc) return rc;
+    p.M = (int)g->M;
+    p.N = (int)g->N;
+    p.K = (int)g->K;
+    p.num_m = (int)ceil_div(g->M, BM);
+    p.num_n = (int)ceil_div(g->N, bn);
+    p.num_k = (int)ceil_div(g->K, bk);
+    const uint32_t afmt = g->kind == 0 ? (uint32_t)g->a_fmt : 1u;  // bf16 = 1 in the F16 format table
+    const uint32_t bfmt = g->kind == 0 ? (uint32_t)g->b_fmt : 1u;
+    p.idesc = sm100::make_idesc(afmt, bfmt, g->a_mn != 0, g->b_mn != 0, BM, bn);
+    p.a_scale = g->a_scale;
+    p.b_scale = g->b_scale;
+    p.out = g->out;
+    p.ldo = g->ldo;
+    p.res = reinterpret_cast<const uint16_t*>(g->res);
+    p.ldr = g->ldr;
+    p.sr_seed = g->sr_seed;
+    p.sr_stream = g->sr_stream;
+    p.sr_base = g->sr_base;
+    const int tiles = p.num_m * p.num_n;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, s);
+}

@@ -1,0 +1,93 @@
+"""Thin torch-facing wrappers over the stateless C-ABI kernels (qtk_*).
+
+torch is used only for device allocation and the current stream; every
+computation runs in the native library.  Tensors must already be on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _lib
+
+E4M3, E5M2 = 0, 1
+EPI_BF16, EPI_F32, EPI_BF16_RES, EPI_BF16_ACC, EPI_F32_ACC = 0, 1, 2, 3, 4
+
+
+def _p(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _s() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _need_cuda(*ts: torch.Tensor) -> None:
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("qtrain-b200 kernels take CUDA tensors (no CPU fallback)")
+
+
+def absmax(x: torch.Tensor, slot: torch.Tensor | None = None) -> torch.Tensor:
+    """Returns a 1-element int32 tensor holding the f32 bit pattern of max|x|."""
+    _need_cuda(x)
+    if slot is None:
+        slot = torch.zeros(1, dtype=torch.int32, device=x.device)
+    if x.dtype == torch.bfloat16:
+        rc = _lib.lib().qtk_absmax_bf16(_p(x), x.numel(), _p(slot), _s())
+    elif x.dtype == torch.float32:
+        rc = _lib.lib().qtk_absmax_f32(_p(x), x.numel(), _p(slot), _s())
+    else:
+        raise TypeError(x.dtype)
+    _lib.check(rc, "qtk_absmax")
+    return slot
+
+
+def amax_value(slot: torch.Tensor) -> float:
+    return slot.view(torch.float32).item()
+
+
+def quantize(x: torch.Tensor, kind: int, slot: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    _need_cuda(x)
+    codes = torch.empty(x.shape, dtype=torch.uint8, device=x.device)
+    scale = torch.empty(1, dtype=torch.float32, device=x.device)
+    rc = _lib.lib().qtk_quantize_bf16(_p(x), x.numel(), kind, _p(slot), _p(codes), _p(scale), _s())
+    _lib.check(rc, "qtk_quantize_bf16")
+    return codes, scale
+
+
+def quantize_transpose(x: torch.Tensor, kind: int, slot: torch.Tensor, with_rowmajor: bool = False):
+    _need_cuda(x)
+    rows, cols = x.shape
+    ct = torch.empty((cols, rows), dtype=torch.uint8, device=x.device)
+    crm = torch.empty((rows, cols), dtype=torch.uint8, device=x.device) if with_rowmajor else None
+    scale = torch.empty(1, dtype=torch.float32, device=x.device)
+    rc = _lib.lib().qtk_quantize_transpose_bf16(_p(x), rows, cols, kind, _p(slot), _p(ct), _p(crm), _p(scale), _s())
+    _lib.check(rc, "qtk_quantize_transpose_bf16")
+    return ct, crm, scale
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool = False, b_mn: bool = False,
+         a_fmt: int = E4M3, b_fmt: int = E4M3, a_scale: torch.Tensor | None = None,
+         b_scale: torch.Tensor | None = None, epi: int = EPI_BF16, out: torch.Tensor | None = None,
+         res: torch.Tensor | None = None, sr: tuple[int, int, int] = (0, 0, 0), bn: int = 0) -> torch.Tensor:
+    """D[m,n] = sum_k A[m,k] B[n,k].  A stored [M][K] (a_mn=False) or [K][M]
+    (a_mn=True); likewise B.  uint8 operands are FP8 codes, bf16 operands BF16."""
+    _need_cuda(a, b)
+    kind = 0 if a.dtype == torch.uint8 else 1
+    if out is None:
+        dt = torch.float32 if epi == EPI_F32 else torch.bfloat16
+        out = torch.empty((M, N), dtype=dt, device=a.device)
+    g = _lib.QtkGemm()
+    g.kind, g.a_fmt, g.b_fmt, g.a_mn, g.b_mn = kind, a_fmt, b_fmt, int(a_mn), int(b_mn)
+    g.M, g.N, g.K = M, N, K
+    g.a, g.lda = _p(a), a.stride(0)
+    g.b, g.ldb = _p(b), b.stride(0)
+    g.a_scale, g.b_scale = _p(a_scale), _p(b_scale)
+    g.epi, g.out, g.ldo = epi, _p(out), out.stride(0)
+    g.res, g.ldr = _p(res), (res.stride(0) if res is not None else 0)
+    g.sr_seed, g.sr_stream, g.sr_base = sr
+    g.bn = bn
+    _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
+    return out
