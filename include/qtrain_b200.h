@@ -80,9 +80,148 @@ typedef struct QtkGemm {
     int64_t ldr;
     uint64_t sr_seed, sr_stream, sr_base; /* EPI_*_ACC stochastic-rounding key           */
     int bn;             /* N tile: 128 or 256 (0 = auto)                                   */
+    const void* a2;     /* optional split-A operand (same layout/ld as A): D = A.B + A2.B, */
+                        /* used for f32-precision operands carried as bf16 hi + lo pairs    */
 } QtkGemm;
 
 int qtk_gemm(const QtkGemm* g, cudaStream_t s);
+
+/* ------------------------------------------------------------------------- */
+/* fused block ops (src/tensorops.cpp, src/model.cpp)                          */
+/* ------------------------------------------------------------------------- */
+
+/* embedding gather + (inputs, targets) split of B*(T+1) token ids
+ * (src/model.cpp:316-331); *err = 2 on an out-of-range id. */
+int qtk_embed_fwd(const int32_t* tokens, int B, int T, const void* embed, int d, int64_t V, void* r, int32_t* inputs,
+                  int32_t* targets, int* err, cudaStream_t s);
+
+/* rmsnorm_residual_fused (src/tensorops.cpp:61-86): nr = x ? bf16(x+res) : res;
+ * normed = bf16((nr*inv)*gamma); absmax(normed) -> *amax (may be NULL).
+ * Sequential per-row f32 sum of squares == the reference bitwise. */
+int qtk_rmsnorm_fwd(const void* x, const void* res, const void* gamma, int64_t rows, int d, float eps, void* nr_out,
+                    void* normed, float* inv_out, uint32_t* amax, cudaStream_t s);
+
+/* rmsnorm_residual_backward (src/tensorops.cpp:88-112).  dgamma_part needs
+ * qtk_rmsnorm_bwd_partials(rows, d) x d floats; dgamma (d floats) is their
+ * fixed-order column sum. */
+int qtk_rmsnorm_bwd_partials(int64_t rows, int d);
+int qtk_rmsnorm_bwd(const void* nr, const void* gamma, int64_t rows, int d, float eps, const void* dy,
+                    const void* d_extra, void* d_in, float* dgamma_part, float* dgamma, uint32_t* amax,
+                    cudaStream_t s);
+
+/* rope_apply (src/model.cpp:171-191) in place over the first n_rot_heads heads
+ * of each (rows, qkv_dim) row; cs_tab = T x hd/2 float2 {cos, sin} built on the
+ * host with the reference's powf/cosf/sinf.  amax (optional) covers the whole
+ * row (d_qkv quantization). */
+int qtk_rope(void* qkv, int64_t rows, int T, int n_rot_heads, int hd, int qkv_dim, const void* cs_tab, int backward,
+             uint32_t* amax, cudaStream_t s);
+
+/* swiglu_fused / swiglu_backward (src/tensorops.cpp:114-153) + fused absmax. */
+int qtk_swiglu_fwd(const void* gu, int64_t rows, int H, void* h, uint32_t* amax, cudaStream_t s);
+int qtk_swiglu_bwd(const void* gu, const void* dh, int64_t rows, int H, void* dgu, uint32_t* amax, cudaStream_t s);
+
+/* GradAccumulator::accumulate for an f32 gradient (src/model.cpp:455-462). */
+int qtk_sr_accumulate_f32(void* buf, const float* g, int64_t n, uint64_t seed, uint64_t stream, uint64_t base,
+                          cudaStream_t s);
+
+/* embedding_backward_sorted (src/tensorops.cpp:317-342) + bf16 round + accumulate. */
+size_t qtk_embed_sort_scratch_bytes(int n, int64_t V);
+int qtk_embed_sort(const int32_t* ids, int n, int64_t V, void* scratch, size_t scratch_bytes, int32_t* sorted_pos,
+                   int32_t* seg_tok, int32_t* seg_off, int* nseg, cudaStream_t s);
+int qtk_embed_bwd(const int32_t* sorted_pos, const int32_t* seg_off, const int32_t* seg_tok, const int* nseg_dev,
+                  int max_seg, const void* d_r, int d, void* grad, uint64_t seed, uint64_t stream, uint64_t base,
+                  cudaStream_t s);
+
+/* causal GQA attention (sdpa_chunked / sdpa_chunked_backward,
+ * src/tensorops.cpp:191-303) on the (B*T, qkv_dim) RoPE'd tensor. */
+int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
+                 float* out32, float* lse, uint32_t* amax, cudaStream_t s);
+int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv, int B,
+                 int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, cudaStream_t s);
+
+/* fused_cross_entropy_chunked softmax stage (src/tensorops.cpp:367-393):
+ * per-row loss and dlogits from f32 logits; dlogits (f32 in the reference) is
+ * written as bf16 hi + lo parts (either may be NULL). */
+int qtk_ce_softmax(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets, float inv_n,
+                   void* dlogits, void* dlogits_lo, int64_t ldd, float* loss_rows, cudaStream_t s);
+int qtk_loss_reduce(const float* loss_rows, int64_t n, float inv_n, float* out, float* accum, cudaStream_t s);
+
+/* optimizer (src/optim.cpp:37-110).  segs: device array of per-tensor segment
+ * records (size qtk_seg_size()). */
+int qtk_seg_size(void);
+int qtk_grad_sumsq(const void* grad, int grad_f32, const void* segs, int nseg, int64_t nblk, double* partials,
+                   double* scratch, double* out, cudaStream_t s);
+int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,
+                  int nseg, int64_t total, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
+                  const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
+                  uint32_t* seg_amax, cudaStream_t s);
+
+/* ------------------------------------------------------------------------- */
+/* device-resident session: the reference operator API                        */
+/* ------------------------------------------------------------------------- */
+
+/* ModelConfig (include/qtrain/model.hpp:24-39) */
+typedef struct QtModelConfig {
+    int n_layers, d_model, d_ff, n_heads, n_kv_heads;
+    int64_t vocab;
+    int seq_len;
+} QtModelConfig;
+
+/* PrecisionMap (model.hpp:47-57): block_matmuls 0 = FP8_E4M3, 1 = BF16;
+ * backward_grads 0 = E4M3, 1 = E5M2.  The device path runs FP8 only. */
+typedef struct QtPrecisionMap {
+    int block_matmuls, backward_grads, f32_debug;
+} QtPrecisionMap;
+
+/* RunPlan subset (include/qtrain/memplan.hpp:54-67) + ChunkSpec (model.hpp:158-161).
+ * recompute_bits: RecomputeSet bits (model.hpp:59-80). */
+typedef struct QtRunPlan {
+    int micro_batch, ga_steps, recompute_bits;
+    int64_t lmhead_chunk_tokens, attn_chunk_rows;
+    int shard_weights, shard_grads, bf16_moments;
+} QtRunPlan;
+
+/* AdamWHyper (include/qtrain/optim.hpp:20-26) + RunManifest::max_grad_norm */
+typedef struct QtAdamW {
+    float lr, beta1, beta2, eps, weight_decay, max_grad_norm;
+} QtAdamW;
+
+typedef struct qt_session qt_session;
+
+const char* qt_last_error(void);
+int qt_nccl_unique_id(void* out128);
+int qt_session_create(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan, const QtAdamW* hyper,
+                      uint64_t seed, int rank, int world, const void* nccl_id, int device, qt_session** out);
+void qt_session_destroy(qt_session* s);
+void* qt_session_stream(qt_session* s);
+size_t qt_session_bytes(qt_session* s);
+int qt_num_params(qt_session* s);
+int qt_param_info(qt_session* s, int i, const char** name, int64_t* numel);
+int qt_param_upload(qt_session* s, int i, const float* host);
+int qt_param_download(qt_session* s, int i, float* host);
+int qt_grad_download(qt_session* s, int i, float* host);
+int qt_moments_download(qt_session* s, int i, float* m, float* v);
+int qt_moments_upload(qt_session* s, int i, const float* m, const float* v, int64_t step_count);
+int qt_init_params(qt_session* s, uint64_t seed);                 /* init_params, model.cpp:67-86   */
+int qt_build_step_context(qt_session* s);                          /* build_step_context, :88-107    */
+int qt_forward(qt_session* s, const int32_t* tokens_dev, int64_t n_tokens, int64_t batch, int with_grads,
+               float* loss_host);                                  /* model_forward, :297-352        */
+int qt_backward(qt_session* s, uint64_t micro_step);               /* model_backward + accumulate    */
+int qt_zero_grads(qt_session* s);
+int qt_grad_norm(qt_session* s, double* norm_host);                /* global_grad_norm, optim.cpp:87-105 */
+int qt_adamw_step(qt_session* s, float grad_scale);                /* (sharded_)adamw_step           */
+int qt_train_step(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch, int64_t step,
+                  float max_grad_norm, float* loss_host, float* norm_host); /* trainer.cpp:64-110 */
+int qt_upload_tokens(qt_session* s, const int32_t* host, int64_t n, int32_t** dev_out);
+int qt_sync(qt_session* s);
+int qt_forward_stats(qt_session* s, float* out);
+int qt_saved_raw(qt_session* s, int layer, const char* site, void* host, int64_t* bytes, int* dtype);
+int qt_scales(qt_session* s, int which, float* out);
+int qt_weight_codes(qt_session* s, int layer, int which, uint8_t* host);
+int qt_set_profile(qt_session* s, int on);
+int qt_profile_read(qt_session* s, int ncat, double* ms, int64_t* launches, double* work);
+int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_worker);
+uint64_t qt_fnv1a64(const char* s);
 
 #ifdef __cplusplus
 }

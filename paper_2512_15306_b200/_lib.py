@@ -22,7 +22,7 @@ class QtkGemm(C.Structure):
         ("a", c_vp), ("lda", c_i64), ("b", c_vp), ("ldb", c_i64),
         ("a_scale", c_vp), ("b_scale", c_vp),
         ("epi", C.c_int), ("out", c_vp), ("ldo", c_i64), ("res", c_vp), ("ldr", c_i64),
-        ("sr_seed", c_u64), ("sr_stream", c_u64), ("sr_base", c_u64), ("bn", C.c_int),
+        ("sr_seed", c_u64), ("sr_stream", c_u64), ("sr_base", c_u64), ("bn", C.c_int), ("a2", c_vp),
     ]
 
 
@@ -33,6 +33,17 @@ _SIGS = {
     "qtk_quantize_bf16": (C.c_int, [c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp, c_vp]),
     "qtk_quantize_transpose_bf16": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "qtk_gemm": (C.c_int, [C.POINTER(QtkGemm), c_vp]),
+    "qtk_ce_softmax": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "qtk_attn_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_i64, c_vp, c_vp,
+                               c_vp, c_vp]),
+    "qtk_attn_bwd": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                               C.c_int, c_vp, c_vp]),
+    "qtk_rmsnorm_fwd": (C.c_int, [c_vp, c_vp, c_vp, c_i64, C.c_int, C.c_float, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "qtk_rmsnorm_bwd": (C.c_int, [c_vp, c_vp, c_i64, C.c_int, C.c_float, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "qtk_rmsnorm_bwd_partials": (C.c_int, [c_i64, C.c_int]),
+    "qtk_swiglu_fwd": (C.c_int, [c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp]),
+    "qtk_swiglu_bwd": (C.c_int, [c_vp, c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp]),
+    "qtk_rope": (C.c_int, [c_vp, c_i64, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, C.c_int, c_vp, c_vp]),
 }
 
 _lib = None

@@ -35,8 +35,10 @@ constexpr int BM = 128;
 struct alignas(64) Params {
     CUtensorMap ta;
     CUtensorMap tb;
+    CUtensorMap ta2;  // split-A: D = A.B + A2.B (the K loop runs twice, B repeats)
     int M, N, K;
     int num_m, num_n, num_k;
+    int split_a;
     uint32_t idesc;
     const float* a_scale;
     const float* b_scale;
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.ta);
         tma_prefetch(&p.tb);
+        if (p.split_a) tma_prefetch(&p.ta2);
     }
     if (warp == 1 && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const int tiles = p.num_m * p.num_n;
+    const int kiters = p.split_a ? 2 * p.num_k : p.num_k;
 
     if (warp == 0 && lane == 0) {
         // ===== TMA producer =====
@@ -177,18 +181,20 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         uint32_t phase = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
             const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
-            for (int kb = 0; kb < p.num_k; ++kb) {
+            for (int kb = 0; kb < kiters; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = base + stage * C::STAGE;
                 uint8_t* sb = sa + C::A_BYTES;
                 mbar_arrive_expect_tx(&full[stage], C::STAGE);
-                const int k0 = kb * C::BK;
+                const bool second = kb >= p.num_k;
+                const CUtensorMap* tA = second ? &p.ta2 : &p.ta;
+                const int k0 = (second ? kb - p.num_k : kb) * C::BK;
                 if constexpr (!A_MN) {
-                    tma_load_2d(&p.ta, &full[stage], sa, k0, m0);
+                    tma_load_2d(tA, &full[stage], sa, k0, m0);
                 } else {
 #pragma unroll
                     for (int i = 0; i < BM * C::ELEM / 128; ++i)
-                        tma_load_2d(&p.ta, &full[stage], sa + i * C::BK * 128, m0 + i * (128 / C::ELEM), k0);
+                        tma_load_2d(tA, &full[stage], sa + i * C::BK * 128, m0 + i * (128 / C::ELEM), k0);
                 }
                 if constexpr (!B_MN) {
                     tma_load_2d(&p.tb, &full[stage], sb, k0, n0);
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             mbar_wait(&tempty[acc], aphase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem + acc * BN;
-            for (int kb = 0; kb < p.num_k; ++kb) {
+            for (int kb = 0; kb < kiters; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 const uint32_t sa = smem_u32(base + stage * C::STAGE);
@@ -384,6 +390,15 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     else
         rc = make_tmap(&p.tb, g->b, elem, g->N, g->K, g->ldb, 128 / elem, bk);
     if (rc) return rc;
+    if (g->a2) {
+        if (reinterpret_cast<uintptr_t>(g->a2) & 15) return 1;
+        if (!g->a_mn)
+            rc = make_tmap(&p.ta2, g->a2, elem, g->K, g->M, g->lda, bk, BM);
+        else
+            rc = make_tmap(&p.ta2, g->a2, elem, g->M, g->K, g->lda, 128 / elem, bk);
+        if (rc) return rc;
+        p.split_a = 1;
+    }
     p.M = (int)g->M;
     p.N = (int)g->N;
     p.K = (int)g->K;

@@ -1,0 +1,1240 @@
+// Device-resident training session: the B200 implementation of the
+// reference's model/optimizer entry points (include/qtrain/model.hpp:125-211,
+// include/qtrain/optim.hpp:55-77) and of one trainer step
+// (src/trainer.cpp:64-131), driving the qtk_* kernels on one CUDA stream.
+//
+// HBM layout (one arena, allocated once at creation):
+//   params   bf16, every tensor in for_each_param order (model.hpp:107-121),
+//            each padded to W*pw elements (ZeRO-1 shard layout, comms.cpp:69-73)
+//   grads    bf16 GradAccumulator buffers, same layout (SR-accumulated by the
+//            wgrad GEMM epilogues)
+//   m, v     f32 (or bf16-SR) AdamW moments for this rank's shard only
+//   wcodes   E4M3 codes of the four block weights per layer (StepContext)
+//   per layer saved activations (kept sites) + shared scratch (dropped sites)
+//   CE       f32 logits and bf16 dlogits for the whole micro-batch
+#include "common.cuh"
+#include "kernels.h"
+#include "nccl_dl.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace qtb {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+thread_local std::string g_last_error;
+
+struct QtError : std::runtime_error {
+    int code;
+    QtError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define QT_CHECK_CUDA(x)                                                                              \
+    do {                                                                                              \
+        cudaError_t e_ = (x);                                                                         \
+        if (e_ != cudaSuccess) throw QtError(3, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                                    " at " #x);                                       \
+    } while (0)
+#define QT_CHECK_K(x)                                                                                 \
+    do {                                                                                              \
+        int rc_ = (x);                                                                                \
+        if (rc_ != 0) throw QtError(rc_ == 1 ? 1 : 3, std::string("kernel launch failed (") +        \
+                                                          std::to_string(rc_) + "): " #x);            \
+    } while (0)
+
+uint64_t fnv1a64(const std::string& s) {
+    uint64_t h = 0xCBF29CE484222325ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 0x100000001B3ull;
+    }
+    return h;
+}
+
+// layout-compatible with qtb::Seg in ce_optim.cu (size checked at runtime)
+struct SegH {
+    int64_t off, n, gstart, gnumel;
+    uint64_t sm, sv, sw;
+    int64_t blk0, poff;
+};
+
+// ---------------------------------------------------------------------------
+// small session kernels
+// ---------------------------------------------------------------------------
+// normal_init (src/model.cpp:56-65) with rng_normal (src/numerics.cpp:216-226)
+__global__ void init_normal_kernel(uint16_t* t, int64_t n, float std_, uint64_t seed, uint64_t stream) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t c = (uint64_t)i;
+        const double u1 = ((double)rng_uniform(seed, stream, 2 * c) + 1.0) * 0x1.0p-32;
+        const double u2 = (double)rng_uniform(seed, stream, 2 * c + 1) * 0x1.0p-32;
+        const double r = sqrt(-2.0 * log(u1));
+        const float z = (float)(r * cos(2.0 * 3.14159265358979323846 * u2));
+        t[i] = f2bfbits(__fmul_rn(std_, z));
+    }
+}
+__global__ void fill_bf16_kernel(uint16_t* t, int64_t n, float v) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        t[i] = f2bfbits(v);
+}
+__global__ void f32_to_bf16_kernel(const float* in, uint16_t* out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = f2bfbits(in[i]);
+}
+__global__ void bf16_to_f32_kernel(const uint16_t* in, float* out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = bfbits2f(in[i]);
+}
+// trainer.cpp:105-107 + optim.cpp:107-110: norm = sqrt(ssq)*mean_scale,
+// clip = min(1, max/norm), grad_scale = mean_scale*clip
+__global__ void finalize_scale_kernel(const double* ssq, float mean_scale, float max_norm, float* grad_scale,
+                                      double* norm_out) {
+    const double norm = sqrt(*ssq) * (double)mean_scale;
+    float clip = 1.0f;
+    if (!(max_norm <= 0.0f || norm <= (double)max_norm)) clip = (float)((double)max_norm / norm);
+    *grad_scale = __fmul_rn(mean_scale, clip);
+    *norm_out = norm;
+}
+__global__ void set_scale_kernel(float* p, float v) { *p = v; }
+// cross-worker sum in ascending worker order, plain f32 (src/trainer.cpp:95-102)
+__global__ void ordered_sum_kernel(const uint16_t* __restrict__ recv, int W, int64_t n, float* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float s = bfbits2f(recv[i]);
+        for (int w = 1; w < W; ++w) s = __fadd_rn(s, bfbits2f(recv[(int64_t)w * n + i]));
+        out[i] = s;
+    }
+}
+
+inline int grid_for(int64_t n, int per = 256) { return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n, per), 1), 16 * kNumSMs); }
+
+// ---------------------------------------------------------------------------
+// session
+// ---------------------------------------------------------------------------
+enum Site { S_N1 = 0, S_ATT = 1, S_N2 = 2, S_H = 3 };
+enum GSite { G_DR = 0, G_DGU = 1, G_DAO = 2, G_DQKV = 3 };
+enum WIdx { W_QKV = 0, W_O = 1, W_GU = 2, W_DOWN = 3 };
+
+struct ParamT {
+    std::string name;
+    std::vector<int64_t> shape;
+    int64_t numel = 0, off = 0, padded = 0, pw = 0;
+    uint64_t s_acc = 0, s_m = 0, s_v = 0, s_w = 0, s_init = 0;
+};
+
+struct LayerBufs {
+    uint16_t* r_in = nullptr;
+    uint8_t* n1c = nullptr;
+    uint16_t* qkv = nullptr;
+    uint16_t* att = nullptr;
+    float* att32 = nullptr;  // unrounded attention output (sdpa backward's orow, tensorops.cpp:278-281)
+    uint8_t* attc = nullptr;
+    float* lse = nullptr;
+    uint16_t* r_mid = nullptr;
+    uint8_t* n2c = nullptr;
+    uint16_t* gu = nullptr;
+    uint8_t* hc = nullptr;
+    bool keep_all = true;
+};
+
+struct ProfRec {
+    int cat;
+    cudaEvent_t a, b;
+    double work;
+};
+
+class Session {
+   public:
+    QtModelConfig cfg;
+    QtPrecisionMap prec;
+    QtRunPlan plan;
+    QtAdamW hyper;
+    uint64_t seed;
+    int rank, world;
+    cudaStream_t st = nullptr;
+    ncclComm_t comm = nullptr;
+
+    int L, d, F, Hh, H, Hkv, hd, q, T;
+    int64_t V, Mmax;
+    std::vector<ParamT> P;
+    std::map<std::string, int> pidx;
+    int64_t p_total = 0;   // padded elements of the flat param buffer
+    int64_t shard_total = 0;
+    int64_t step_count = 0;  // completed optimizer steps (OptimState::step_count)
+
+    // arena
+    uint8_t* arena = nullptr;
+    size_t arena_bytes = 0;
+    uint16_t* params = nullptr;
+    uint16_t* grads = nullptr;
+    float* m32 = nullptr;
+    float* v32 = nullptr;
+    uint16_t* m16 = nullptr;
+    uint16_t* v16 = nullptr;
+    float* gshard = nullptr;      // f32 reduced grads of this rank's shard (W>1)
+    uint16_t* recvbuf = nullptr;  // W x shard_total bf16
+    std::vector<uint8_t*> wcodes;  // L*4
+    std::vector<LayerBufs> lb;
+    uint16_t *s_n1 = nullptr, *s_attn_out = nullptr, *s_n2 = nullptr, *s_h = nullptr, *normed_final = nullptr;
+    uint16_t *d_r = nullptr, *d_h = nullptr, *d_gu = nullptr, *d_n = nullptr, *d_ao = nullptr, *d_att = nullptr,
+             *d_qkv = nullptr, *d_hidden = nullptr;
+    uint8_t* gcodes = nullptr;  // grad-kind codes scratch (M x max(F, q))
+    float* logits = nullptr;
+    uint16_t* dlogits = nullptr;
+    uint16_t* dlogits_lo = nullptr;
+    float* loss_rows = nullptr;
+    float* dgamma_part = nullptr;
+    float* dgamma = nullptr;
+    float* Dv = nullptr;
+    float2* rope_tab = nullptr;
+    int32_t *tok_buf = nullptr, *inputs = nullptr, *targets = nullptr, *sorted_pos = nullptr, *seg_tok = nullptr,
+            *seg_off = nullptr;
+    int* nseg = nullptr;
+    void* sort_scratch = nullptr;
+    size_t sort_scratch_bytes = 0;
+    double* norm_partials = nullptr;
+    double* norm_scratch = nullptr;
+    int64_t norm_blocks = 0;
+    SegH* segs_dev = nullptr;
+    int nsegs = 0;
+    // device scalars
+    uint32_t* act_amax = nullptr;  // L*4
+    float* act_scale = nullptr;    // L*4
+    uint32_t* w_amax = nullptr;    // L*4
+    float* w_scale = nullptr;      // L*4
+    uint32_t* g_amax = nullptr;    // L*4
+    float* g_scale = nullptr;      // L*4
+    uint32_t* fin_amax = nullptr;
+    float* loss_dev = nullptr;     // per micro-batch losses (ga_steps)
+    double* ssq_dev = nullptr;
+    double* norm_dev = nullptr;
+    float* gscale_dev = nullptr;
+    int* err_dev = nullptr;
+    float* scratch_f32 = nullptr;  // param download staging
+
+    // current micro-batch
+    int curB = 0, curT = 0;
+    int64_t curM = 0;
+    bool have_fwd = false, fwd_with_grads = false;
+
+    // profiling
+    bool prof_on = false;
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+
+    Session(const QtModelConfig& c, const QtPrecisionMap& p, const QtRunPlan& pl, const QtAdamW& h, uint64_t sd, int rk,
+            int ws, const void* nccl_id, int device)
+        : cfg(c), prec(p), plan(pl), hyper(h), seed(sd), rank(rk), world(ws) {
+        validate();
+        QT_CHECK_CUDA(cudaSetDevice(device));
+        QT_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        L = c.n_layers;
+        d = c.d_model;
+        F = c.d_ff;
+        Hh = c.d_ff / 2;
+        H = c.n_heads;
+        Hkv = c.n_kv_heads;
+        hd = d / H;
+        q = d + 2 * Hkv * hd;
+        V = c.vocab;
+        T = c.seq_len;
+        Mmax = (int64_t)std::max(1, pl.micro_batch) * T;
+        build_params();
+        allocate();
+        build_segments();
+        build_rope_table();
+        if (world > 1) {
+            auto& api = NcclApi::get();
+            if (!api.ok) throw QtError(3, "world > 1 needs NCCL (libnccl.so.2 not loadable)");
+            if (!nccl_id) throw QtError(1, "world > 1 needs an NCCL unique id");
+            ncclUniqueId id;
+            std::memcpy(&id, nccl_id, sizeof(id));
+            ncclResult_t r = api.CommInitRank(&comm, world, id, rank);
+            if (r != ncclSuccess) throw QtError(3, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+        }
+        QT_CHECK_CUDA(cudaStreamSynchronize(st));
+    }
+
+    ~Session() {
+        if (comm) NcclApi::get().CommDestroy(comm);
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        if (arena) cudaFree(arena);
+        if (st) cudaStreamDestroy(st);
+    }
+
+    void validate() {
+        // ModelConfig::validate (src/model.cpp:12-17)
+        if (cfg.d_model % cfg.n_heads != 0) throw QtError(1, "ModelConfig: d_model % n_heads != 0");
+        if (cfg.n_heads % cfg.n_kv_heads != 0) throw QtError(1, "ModelConfig: n_heads % n_kv_heads != 0");
+        if (cfg.d_ff % 2 != 0) throw QtError(1, "ModelConfig: d_ff must be even (gate | up halves)");
+        if (cfg.n_layers < 1 || cfg.vocab < 2 || cfg.seq_len < 1) throw QtError(1, "ModelConfig: degenerate");
+        if (prec.block_matmuls != 0 || prec.f32_debug)
+            throw QtError(1, "qtrain-b200 runs the FP8 block-matmul path only (BF16 / f32_debug modes are oracle-only)");
+        const int hd_ = cfg.d_model / cfg.n_heads;
+        if (hd_ != 32 && hd_ != 64 && hd_ != 128) throw QtError(1, "head_dim must be 32, 64 or 128");
+        if (cfg.d_model % 16 || cfg.d_ff % 32) throw QtError(1, "d_model % 16 and d_ff % 32 must be 0 (TMA/vector alignment)");
+        if (plan.micro_batch < 1 || plan.ga_steps < 1) throw QtError(1, "RunPlan: micro_batch/ga_steps must be >= 1");
+        if (world < 1 || rank < 0 || rank >= world) throw QtError(1, "bad rank/world");
+    }
+
+    void add_param(const std::string& name, std::vector<int64_t> shape) {
+        ParamT t;
+        t.name = name;
+        t.shape = shape;
+        t.numel = 1;
+        for (auto s : shape) t.numel *= s;
+        const int64_t unit = 256 * (int64_t)world;  // shard_layout (src/comms.cpp:69-73)
+        t.padded = ceil_div(t.numel, unit) * unit;
+        t.pw = t.padded / world;
+        t.off = p_total;
+        p_total += t.padded;
+        t.s_acc = fnv1a64("gradaccum/" + name);
+        t.s_m = fnv1a64("adamw/" + name + "/m");
+        t.s_v = fnv1a64("adamw/" + name + "/v");
+        t.s_w = fnv1a64("adamw/" + name + "/w");
+        t.s_init = fnv1a64("init/" + name);
+        pidx[name] = (int)P.size();
+        P.push_back(t);
+    }
+
+    void build_params() {
+        add_param("embed", {V, d});
+        for (int l = 0; l < L; ++l) {
+            const std::string pre = "layers." + std::to_string(l) + ".";
+            add_param(pre + "ln1_g", {d});
+            add_param(pre + "w_qkv", {q, d});
+            add_param(pre + "w_o", {d, d});
+            add_param(pre + "ln2_g", {d});
+            add_param(pre + "w_gate_up", {F, d});
+            add_param(pre + "w_down", {d, Hh});
+        }
+        add_param("final_g", {d});
+        add_param("lm_head", {V, d});
+        shard_total = 0;
+        for (auto& t : P) shard_total += t.pw;
+    }
+    const ParamT& par(const std::string& n) const { return P.at(pidx.at(n)); }
+    uint16_t* pptr(const std::string& n) { return params + par(n).off; }
+    uint16_t* gptr(const std::string& n) { return grads + par(n).off; }
+    int lp(int l, int k) const { return 1 + 6 * l + k; }  // k: 0 ln1 1 qkv 2 o 3 ln2 4 gu 5 down
+
+    bool keep(int site) const {
+        // KeepMask::from (src/model.cpp:221-235); RecomputeSite bits: 0 SwiGLU 1 RMSNorm 2 Attention 3 QKV 4 FFN 5 Block
+        const int b = plan.recompute_bits;
+        const bool block = b & (1 << 5);
+        if (block) return false;
+        switch (site) {
+            case 0: return !(b & (1 << 1));                     // n1
+            case 1: return !(b & (1 << 3));                     // qkv
+            case 2: return !(b & (1 << 2));                     // att
+            case 3: return true;                                // r_mid
+            case 4: return !(b & (1 << 1));                     // n2
+            case 5: return !(b & (1 << 4));                     // gate_up
+            case 6: return !(b & (1 << 4)) && !(b & (1 << 0));  // h
+        }
+        return true;
+    }
+
+    void allocate() {
+        struct Req {
+            void** p;
+            size_t bytes;
+        };
+        std::vector<Req> reqs;
+        auto req = [&](auto** p, size_t bytes) { reqs.push_back({reinterpret_cast<void**>(p), bytes}); };
+        const int64_t M = Mmax;
+        req(&params, p_total * 2);
+        req(&grads, p_total * 2);
+        if (plan.bf16_moments) {
+            req(&m16, shard_total * 2);
+            req(&v16, shard_total * 2);
+        } else {
+            req(&m32, shard_total * 4);
+            req(&v32, shard_total * 4);
+        }
+        if (world > 1) {
+            req(&gshard, shard_total * 4);
+            req(&recvbuf, (size_t)world * shard_total * 2);
+        }
+        wcodes.assign((size_t)L * 4, nullptr);
+        for (int l = 0; l < L; ++l) {
+            req(&wcodes[l * 4 + W_QKV], (size_t)q * d);
+            req(&wcodes[l * 4 + W_O], (size_t)d * d);
+            req(&wcodes[l * 4 + W_GU], (size_t)F * d);
+            req(&wcodes[l * 4 + W_DOWN], (size_t)d * Hh);
+        }
+        lb.assign(L + 1, LayerBufs());
+        // shared scratch for dropped sites
+        LayerBufs sc;
+        req(&sc.n1c, M * d);
+        req(&sc.qkv, M * q * 2);
+        req(&sc.att, M * d * 2);
+        req(&sc.att32, M * d * 4);
+        req(&sc.attc, M * d);
+        req(&sc.lse, (size_t)plan.micro_batch * H * T * 4);
+        req(&sc.r_mid, M * d * 2);
+        req(&sc.n2c, M * d);
+        req(&sc.gu, M * F * 2);
+        req(&sc.hc, M * Hh);
+        for (int l = 0; l <= L; ++l) req(&lb[l].r_in, M * d * 2);  // r_in[L] = r_final
+        std::vector<LayerBufs> own(L);
+        for (int l = 0; l < L; ++l) {
+            if (keep(0)) req(&own[l].n1c, M * d);
+            if (keep(1)) req(&own[l].qkv, M * q * 2);
+            if (keep(2)) {
+                req(&own[l].att, M * d * 2);
+                req(&own[l].att32, M * d * 4);
+                req(&own[l].attc, M * d);
+                req(&own[l].lse, (size_t)plan.micro_batch * H * T * 4);
+            }
+            if (keep(3)) req(&own[l].r_mid, M * d * 2);
+            if (keep(4)) req(&own[l].n2c, M * d);
+            if (keep(5)) req(&own[l].gu, M * F * 2);
+            if (keep(6)) req(&own[l].hc, M * Hh);
+        }
+        req(&s_n1, M * d * 2);
+        req(&s_attn_out, M * d * 2);
+        req(&s_n2, M * d * 2);
+        req(&s_h, M * Hh * 2);
+        req(&normed_final, M * d * 2);
+        req(&d_r, M * d * 2);
+        req(&d_h, M * Hh * 2);
+        req(&d_gu, M * F * 2);
+        req(&d_n, M * d * 2);
+        req(&d_ao, M * d * 2);
+        req(&d_att, M * d * 2);
+        req(&d_qkv, M * q * 2);
+        req(&d_hidden, M * d * 2);
+        req(&gcodes, M * std::max(F, q));
+        req(&logits, (size_t)M * V * 4);
+        req(&dlogits, (size_t)M * V * 2);
+        req(&dlogits_lo, (size_t)M * V * 2);
+        req(&loss_rows, M * 4);
+        const int nblk = qtk_rmsnorm_bwd_partials(M, d);
+        req(&dgamma_part, (size_t)nblk * d * 4);
+        req(&dgamma, d * 4);
+        req(&Dv, (size_t)plan.micro_batch * H * T * 4);
+        req(&rope_tab, (size_t)T * (hd / 2) * 8);
+        req(&tok_buf, (size_t)plan.ga_steps * plan.micro_batch * (T + 1) * 4);
+        req(&inputs, M * 4);
+        req(&targets, M * 4);
+        req(&sorted_pos, M * 4);
+        req(&seg_tok, M * 4);
+        req(&seg_off, (M + 1) * 4);
+        req(&nseg, 16);
+        sort_scratch_bytes = qtk_embed_sort_scratch_bytes((int)M, V);
+        req(&sort_scratch, sort_scratch_bytes);
+        // norm partials sized for the largest buffer the norm runs over
+        norm_blocks = 0;
+        for (auto& t : P) norm_blocks += ceil_div(world > 1 ? t.pw : t.numel, 256);
+        req(&norm_partials, norm_blocks * 8);
+        req(&norm_scratch, 1024 * 8);
+        req(&segs_dev, P.size() * sizeof(SegH));
+        req(&act_amax, L * 16);
+        req(&act_scale, L * 16);
+        req(&w_amax, L * 16);
+        req(&w_scale, L * 16);
+        req(&g_amax, L * 16);
+        req(&g_scale, L * 16);
+        req(&fin_amax, 16);
+        req(&loss_dev, std::max(plan.ga_steps, 1) * 4 + 16);
+        req(&ssq_dev, 16);
+        req(&norm_dev, 16);
+        req(&gscale_dev, 16);
+        req(&err_dev, 16);
+        int64_t maxp = 0;
+        for (auto& t : P) maxp = std::max(maxp, t.padded);
+        req(&scratch_f32, maxp * 4);
+
+        size_t total = 0;
+        for (auto& r : reqs) total += (r.bytes + 255) & ~size_t(255);
+        QT_CHECK_CUDA(cudaMalloc(&arena, total));
+        arena_bytes = total;
+        QT_CHECK_CUDA(cudaMemsetAsync(arena, 0, total, st));
+        size_t off = 0;
+        for (auto& r : reqs) {
+            *r.p = arena + off;
+            off += (r.bytes + 255) & ~size_t(255);
+        }
+        for (int l = 0; l < L; ++l) {
+            LayerBufs& b = lb[l];
+            b.n1c = own[l].n1c ? own[l].n1c : sc.n1c;
+            b.qkv = own[l].qkv ? own[l].qkv : sc.qkv;
+            b.att = own[l].att ? own[l].att : sc.att;
+            b.att32 = own[l].att32 ? own[l].att32 : sc.att32;
+            b.attc = own[l].attc ? own[l].attc : sc.attc;
+            b.lse = own[l].lse ? own[l].lse : sc.lse;
+            b.r_mid = own[l].r_mid ? own[l].r_mid : sc.r_mid;
+            b.gu = own[l].gu ? own[l].gu : sc.gu;
+            b.n2c = own[l].n2c ? own[l].n2c : sc.n2c;
+            b.hc = own[l].hc ? own[l].hc : sc.hc;
+            b.keep_all = keep(0) && keep(1) && keep(2) && keep(3) && keep(4) && keep(5) && keep(6);
+        }
+    }
+
+    // AdamW / norm segments for this rank (ZeRO-1 slices when world > 1)
+    void build_segments() {
+        if ((int)sizeof(SegH) != qtk_seg_size()) throw QtError(3, "Seg layout mismatch");
+        std::vector<SegH> segs;
+        int64_t blk = 0, soff = 0;
+        for (auto& t : P) {
+            SegH s{};
+            if (world == 1) {
+                s.off = t.off;
+                s.n = t.numel;
+                s.gstart = 0;
+                s.poff = t.off;
+            } else {
+                const int64_t lo = std::min<int64_t>((int64_t)rank * t.pw, t.numel);
+                const int64_t hi = std::min<int64_t>((int64_t)(rank + 1) * t.pw, t.numel);
+                s.off = soff;
+                s.n = hi - lo;
+                s.gstart = (int64_t)rank * t.pw;
+                s.poff = t.off + (int64_t)rank * t.pw;
+                soff += t.pw;
+            }
+            s.gnumel = t.numel;
+            s.sm = t.s_m;
+            s.sv = t.s_v;
+            s.sw = t.s_w;
+            s.blk0 = blk;
+            blk += ceil_div(s.n, 256);
+            segs.push_back(s);
+        }
+        // norm blocks in name (std::map) order are not needed for the tree sum; layout order is used
+        norm_blocks = blk;
+        nsegs = (int)segs.size();
+        QT_CHECK_CUDA(cudaMemcpyAsync(segs_dev, segs.data(), segs.size() * sizeof(SegH), cudaMemcpyHostToDevice, st));
+        QT_CHECK_CUDA(cudaStreamSynchronize(st));
+    }
+
+    // rope_apply angles (src/model.cpp:178-183) with the reference's own float libm calls
+    void build_rope_table() {
+        const int half = hd / 2;
+        std::vector<float2> tab((size_t)T * half);
+        for (int t = 0; t < T; ++t) {
+            for (int i = 0; i < half; ++i) {
+                const float freq = std::pow(10000.0f, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
+                const float angle = static_cast<float>(t) * freq;
+                tab[(size_t)t * half + i] = make_float2(std::cos(angle), std::sin(angle));
+            }
+        }
+        QT_CHECK_CUDA(cudaMemcpyAsync(rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
+        QT_CHECK_CUDA(cudaStreamSynchronize(st));
+    }
+
+    // ---------------- profiling ----------------
+    int prof_begin() {
+        if (!prof_on) return -1;
+        if (ev_used + 2 > ev_pool.size()) {
+            for (int i = 0; i < 256; ++i) {
+                cudaEvent_t e;
+                cudaEventCreate(&e);
+                ev_pool.push_back(e);
+            }
+        }
+        cudaEvent_t a = ev_pool[ev_used++], b = ev_pool[ev_used++];
+        cudaEventRecord(a, st);
+        prof.push_back({0, a, b, 0.0});
+        return (int)prof.size() - 1;
+    }
+    void prof_end(int h, int cat, double work) {
+        if (h < 0) return;
+        prof[h].cat = cat;
+        prof[h].work = work;
+        cudaEventRecord(prof[h].b, st);
+    }
+
+    // ---------------- GEMM helper ----------------
+    void gemm(int kind, int afmt, int bfmt, bool a_mn, bool b_mn, int64_t M, int64_t N, int64_t K, const void* a,
+              int64_t lda, const void* b, int64_t ldb, const float* as, const float* bs, int epi, void* out,
+              int64_t ldo, const void* res = nullptr, int64_t ldr = 0, uint64_t sr_seed = 0, uint64_t sr_stream = 0,
+              uint64_t sr_base = 0, const void* a2 = nullptr) {
+        QtkGemm g{};
+        g.kind = kind;
+        g.a_fmt = afmt;
+        g.b_fmt = bfmt;
+        g.a_mn = a_mn;
+        g.b_mn = b_mn;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.a = a;
+        g.lda = lda;
+        g.b = b;
+        g.ldb = ldb;
+        g.a_scale = as;
+        g.b_scale = bs;
+        g.epi = epi;
+        g.out = out;
+        g.ldo = ldo;
+        g.res = res;
+        g.ldr = ldr;
+        g.sr_seed = sr_seed;
+        g.sr_stream = sr_stream;
+        g.sr_base = sr_base;
+        g.bn = 0;
+        g.a2 = a2;
+        const int h = prof_begin();
+        QT_CHECK_K(qtk_gemm(&g, st));
+        prof_end(h, kind == 0 ? 0 : 1, 2.0 * M * N * K * (a2 ? 2 : 1));
+    }
+
+    int gkind() const { return prec.backward_grads == 0 ? kE4M3 : kE5M2; }
+
+    // ---------------- StepContext (src/model.cpp:88-107) ----------------
+    void build_step_context() {
+        QT_CHECK_CUDA(cudaMemsetAsync(w_amax, 0, L * 16, st));
+        for (int l = 0; l < L; ++l) {
+            const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
+            for (int k = 0; k < 4; ++k) {
+                const ParamT& t = P[widx[k]];
+                const int h = prof_begin();
+                QT_CHECK_K(qtk_absmax_bf16(params + t.off, t.numel, w_amax + l * 4 + k, st));
+                QT_CHECK_K(qtk_quantize_bf16(params + t.off, t.numel, kE4M3, w_amax + l * 4 + k, wcodes[l * 4 + k],
+                                             w_scale + l * 4 + k, st));
+                prof_end(h, 3, 3.0 * t.numel);
+            }
+        }
+    }
+
+    // ---------------- block forward (src/model.cpp:239-293) ----------------
+    void block_forward(int l, bool record) {
+        LayerBufs& b = lb[l];
+        const int64_t M = curM;
+        uint32_t* am = act_amax + l * 4;
+        float* sc = act_scale + l * 4;
+        const float* ws = w_scale + l * 4;
+        const ParamT& ln1 = P[lp(l, 0)];
+        const ParamT& ln2 = P[lp(l, 3)];
+        int h;
+        // rmsnorm1 (pass-through residual) + N1 absmax
+        h = prof_begin();
+        QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, b.r_in, params + ln1.off, M, d, 1e-6f, nullptr, s_n1, nullptr,
+                                   record ? am + S_N1 : nullptr, st));
+        prof_end(h, 4, 4.0 * M * d);
+        h = prof_begin();
+        QT_CHECK_K(qtk_quantize_bf16(s_n1, M * d, kE4M3, am + S_N1, b.n1c, sc + S_N1, st));
+        prof_end(h, 3, 3.0 * M * d);
+        gemm(0, kE4M3, kE4M3, false, false, M, q, d, b.n1c, d, wcodes[l * 4 + W_QKV], d, sc + S_N1, ws + W_QKV, EPI_BF16,
+             b.qkv, q);
+        h = prof_begin();
+        QT_CHECK_K(qtk_rope(b.qkv, M, curT, H + Hkv, hd, q, rope_tab, 0, nullptr, st));
+        prof_end(h, 5, 4.0 * M * (d + Hkv * hd));
+        h = prof_begin();
+        QT_CHECK_K(qtk_attn_fwd(b.qkv, curB, curT, H, Hkv, hd, q, b.att, d, b.att32, b.lse,
+                                record ? am + S_ATT : nullptr, st));
+        prof_end(h, 6, 4.0 * curB * H * (double)curT * curT / 2 * hd);
+        h = prof_begin();
+        QT_CHECK_K(qtk_quantize_bf16(b.att, M * d, kE4M3, am + S_ATT, b.attc, sc + S_ATT, st));
+        prof_end(h, 3, 3.0 * M * d);
+        gemm(0, kE4M3, kE4M3, false, false, M, d, d, b.attc, d, wcodes[l * 4 + W_O], d, sc + S_ATT, ws + W_O, EPI_BF16,
+             s_attn_out, d);
+        h = prof_begin();
+        QT_CHECK_K(qtk_rmsnorm_fwd(s_attn_out, b.r_in, params + ln2.off, M, d, 1e-6f, b.r_mid, s_n2, nullptr,
+                                   record ? am + S_N2 : nullptr, st));
+        prof_end(h, 4, 8.0 * M * d);
+        h = prof_begin();
+        QT_CHECK_K(qtk_quantize_bf16(s_n2, M * d, kE4M3, am + S_N2, b.n2c, sc + S_N2, st));
+        prof_end(h, 3, 3.0 * M * d);
+        gemm(0, kE4M3, kE4M3, false, false, M, F, d, b.n2c, d, wcodes[l * 4 + W_GU], d, sc + S_N2, ws + W_GU, EPI_BF16,
+             b.gu, F);
+        h = prof_begin();
+        QT_CHECK_K(qtk_swiglu_fwd(b.gu, M, Hh, s_h, record ? am + S_H : nullptr, st));
+        prof_end(h, 5, 2.0 * M * F + 2.0 * M * Hh);
+        h = prof_begin();
+        QT_CHECK_K(qtk_quantize_bf16(s_h, M * Hh, kE4M3, am + S_H, b.hc, sc + S_H, st));
+        prof_end(h, 3, 3.0 * M * Hh);
+        // r_out = bf16(bf16(h . Wdown^T) + r_mid)  (model.cpp:281-283) -> next layer's r_in
+        gemm(0, kE4M3, kE4M3, false, false, M, d, Hh, b.hc, Hh, wcodes[l * 4 + W_DOWN], Hh, sc + S_H, ws + W_DOWN,
+             EPI_BF16_RES, lb[l + 1].r_in, d, b.r_mid, d);
+    }
+
+    // ---------------- model_forward (src/model.cpp:297-352) ----------------
+    void forward(const int32_t* tokens, int64_t n_tokens, int64_t batch, bool with_grads) {
+        if (batch < 1 || n_tokens % batch != 0) throw QtError(1, "model_forward: token count not divisible by batch");
+        const int64_t seq = n_tokens / batch - 1;
+        if (seq < 1 || seq > cfg.seq_len) throw QtError(1, "model_forward: bad sequence length");
+        if (batch * seq > Mmax) throw QtError(1, "model_forward: batch exceeds the session's micro_batch");
+        curB = (int)batch;
+        curT = (int)seq;
+        curM = batch * seq;
+        const int64_t M = curM;
+        QT_CHECK_CUDA(cudaMemsetAsync(act_amax, 0, L * 16, st));
+        QT_CHECK_CUDA(cudaMemsetAsync(fin_amax, 0, 4, st));
+        int h = prof_begin();
+        QT_CHECK_K(qtk_embed_fwd(tokens, curB, curT, params + par("embed").off, d, V, lb[0].r_in, inputs, targets,
+                                 err_dev, st));
+        prof_end(h, 5, 4.0 * M * d);
+        if (with_grads) QT_CHECK_K(qtk_embed_sort(inputs, (int)M, V, sort_scratch, sort_scratch_bytes, sorted_pos,
+                                                  seg_tok, seg_off, nseg, st));
+        for (int l = 0; l < L; ++l) block_forward(l, true);
+        h = prof_begin();
+        QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, lb[L].r_in, pptr("final_g"), M, d, 1e-6f, nullptr, normed_final, nullptr,
+                                   fin_amax, st));
+        prof_end(h, 4, 4.0 * M * d);
+        // fused CE forward (+ dlogits for the backward): logits in f32 (tensorops.cpp:372-376)
+        gemm(1, 0, 0, false, false, M, V, d, normed_final, d, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, logits, V);
+        h = prof_begin();
+        QT_CHECK_K(qtk_ce_softmax(logits, V, M, (int)V, targets, 1.0f / (float)M, with_grads ? dlogits : nullptr,
+                                  with_grads ? dlogits_lo : nullptr, V, loss_rows, st));
+        prof_end(h, 7, (with_grads ? 10.0 : 4.0) * M * V);
+        QT_CHECK_K(qtk_loss_reduce(loss_rows, M, 1.0f / (float)M, loss_dev, nullptr, st));
+        have_fwd = true;
+        fwd_with_grads = with_grads;
+    }
+
+    // ---------------- model_backward + GradAccumulator (src/model.cpp:354-464) ----------------
+    void backward(uint64_t micro_step) {
+        if (!have_fwd || !fwd_with_grads) throw QtError(1, "model_backward: no forward with grads to differentiate");
+        const int64_t M = curM;
+        const uint64_t aseed = seed + (uint64_t)rank;  // trainer.cpp:68-70: worker w accumulates with seed+w
+        const int gk = gkind();
+        int h;
+        // CE backward matmuls: d_hidden = dlogits . lm_w ; d_lm_w = dlogits^T . hidden
+        // (dlogits is f32 in the reference: hi + lo bf16 parts through the split-A GEMM)
+        gemm(1, 0, 0, false, true, M, d, V, dlogits, V, pptr("lm_head"), d, nullptr, nullptr, EPI_BF16, d_hidden, d,
+             nullptr, 0, 0, 0, 0, dlogits_lo);
+        {
+            const ParamT& t = par("lm_head");
+            gemm(1, 0, 0, true, true, V, d, M, dlogits, V, normed_final, d, nullptr, nullptr, EPI_F32_ACC,
+                 grads + t.off, d, nullptr, 0, aseed, t.s_acc, micro_step * (uint64_t)t.numel, dlogits_lo);
+        }
+        // final norm backward (model.cpp:359-363)
+        h = prof_begin();
+        QT_CHECK_CUDA(cudaMemsetAsync(g_amax, 0, L * 16, st));
+        QT_CHECK_K(qtk_rmsnorm_bwd(lb[L].r_in, pptr("final_g"), M, d, 1e-6f, d_hidden, nullptr, d_r, dgamma_part,
+                                   dgamma, g_amax + (L - 1) * 4 + G_DR, st));
+        accumulate_f32(par("final_g"), dgamma, micro_step);
+        prof_end(h, 4, 8.0 * M * d);
+        for (int l = L - 1; l >= 0; --l) {
+            LayerBufs& b = lb[l];
+            if (!b.keep_all) block_forward(l, false);  // replay with cached stats (model.cpp:374-378)
+            uint32_t* ga = g_amax + l * 4;
+            float* gs = g_scale + l * 4;
+            const float* as = act_scale + l * 4;
+            const float* ws = w_scale + l * 4;
+            const ParamT& pq = P[lp(l, 1)];
+            const ParamT& po = P[lp(l, 2)];
+            const ParamT& pg = P[lp(l, 4)];
+            const ParamT& pd = P[lp(l, 5)];
+            // ---- FFN down: dY = d_r
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(d_r, M * d, gk, ga + G_DR, gcodes, gs + G_DR, st));
+            prof_end(h, 3, 3.0 * M * d);
+            gemm(0, gk, kE4M3, true, true, d, Hh, M, gcodes, d, b.hc, Hh, gs + G_DR, as + S_H, EPI_BF16_ACC,
+                 grads + pd.off, Hh, nullptr, 0, aseed, pd.s_acc, micro_step * (uint64_t)pd.numel);
+            gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wcodes[l * 4 + W_DOWN], Hh, gs + G_DR, ws + W_DOWN,
+                 EPI_BF16, d_h, Hh);
+            h = prof_begin();
+            QT_CHECK_K(qtk_swiglu_bwd(b.gu, d_h, M, Hh, d_gu, ga + G_DGU, st));
+            prof_end(h, 5, 2.0 * M * F * 2 + 2.0 * M * Hh);
+            // ---- gate_up
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(d_gu, M * F, gk, ga + G_DGU, gcodes, gs + G_DGU, st));
+            prof_end(h, 3, 3.0 * M * F);
+            gemm(0, gk, kE4M3, true, true, F, d, M, gcodes, F, b.n2c, d, gs + G_DGU, as + S_N2, EPI_BF16_ACC,
+                 grads + pg.off, d, nullptr, 0, aseed, pg.s_acc, micro_step * (uint64_t)pg.numel);
+            gemm(0, gk, kE4M3, false, true, M, d, F, gcodes, F, wcodes[l * 4 + W_GU], d, gs + G_DGU, ws + W_GU, EPI_BF16,
+                 d_n, d);
+            // ---- rmsnorm2 backward: d_attn_out = ... + d_r (model.cpp:393-399)
+            h = prof_begin();
+            QT_CHECK_K(qtk_rmsnorm_bwd(b.r_mid, params + P[lp(l, 3)].off, M, d, 1e-6f, d_n, d_r, d_ao, dgamma_part,
+                                       dgamma, ga + G_DAO, st));
+            accumulate_f32(P[lp(l, 3)], dgamma, micro_step);
+            prof_end(h, 4, 10.0 * M * d);
+            // ---- attention output projection
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(d_ao, M * d, gk, ga + G_DAO, gcodes, gs + G_DAO, st));
+            prof_end(h, 3, 3.0 * M * d);
+            gemm(0, gk, kE4M3, true, true, d, d, M, gcodes, d, b.attc, d, gs + G_DAO, as + S_ATT, EPI_BF16_ACC,
+                 grads + po.off, d, nullptr, 0, aseed, po.s_acc, micro_step * (uint64_t)po.numel);
+            gemm(0, gk, kE4M3, false, true, M, d, d, gcodes, d, wcodes[l * 4 + W_O], d, gs + G_DAO, ws + W_O, EPI_BF16,
+                 d_att, d);
+            // ---- attention backward + inverse RoPE
+            h = prof_begin();
+            QT_CHECK_K(qtk_attn_bwd(b.qkv, b.att32, d_att, d, b.lse, Dv, curB, curT, H, Hkv, hd, q, d_qkv, st));
+            prof_end(h, 8, 10.0 * curB * H * (double)curT * curT / 2 * hd);
+            h = prof_begin();
+            QT_CHECK_K(qtk_rope(d_qkv, M, curT, H + Hkv, hd, q, rope_tab, 1, ga + G_DQKV, st));
+            prof_end(h, 5, 4.0 * M * q);
+            // ---- qkv projection
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(d_qkv, M * q, gk, ga + G_DQKV, gcodes, gs + G_DQKV, st));
+            prof_end(h, 3, 3.0 * M * q);
+            gemm(0, gk, kE4M3, true, true, q, d, M, gcodes, q, b.n1c, d, gs + G_DQKV, as + S_N1, EPI_BF16_ACC,
+                 grads + pq.off, d, nullptr, 0, aseed, pq.s_acc, micro_step * (uint64_t)pq.numel);
+            gemm(0, gk, kE4M3, false, true, M, d, q, gcodes, q, wcodes[l * 4 + W_QKV], d, gs + G_DQKV, ws + W_QKV,
+                 EPI_BF16, d_n, d);
+            // ---- rmsnorm1 backward: d_r = ... + d_attn_out (model.cpp:433-439)
+            h = prof_begin();
+            QT_CHECK_K(qtk_rmsnorm_bwd(b.r_in, params + P[lp(l, 0)].off, M, d, 1e-6f, d_n, d_ao, d_r, dgamma_part,
+                                       dgamma, l > 0 ? g_amax + (l - 1) * 4 + G_DR : nullptr, st));
+            accumulate_f32(P[lp(l, 0)], dgamma, micro_step);
+            prof_end(h, 4, 10.0 * M * d);
+        }
+        // ordered embedding backward, bf16 round, accumulate (model.cpp:442-444)
+        {
+            const ParamT& t = par("embed");
+            h = prof_begin();
+            QT_CHECK_K(qtk_embed_bwd(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, grads + t.off, aseed, t.s_acc,
+                                     micro_step * (uint64_t)t.numel, st));
+            prof_end(h, 5, 4.0 * M * d);
+        }
+    }
+
+    void accumulate_f32(const ParamT& t, const float* g, uint64_t micro_step) {
+        QT_CHECK_K(qtk_sr_accumulate_f32(grads + t.off, g, t.numel, seed + (uint64_t)rank, t.s_acc,
+                                         micro_step * (uint64_t)t.numel, st));
+    }
+
+    // ---------------- cross-rank gradient reduction (ZeRO-1) ----------------
+    // all-to-all of bf16 shards + ascending-rank f32 sum == trainer.cpp:90-103 bitwise
+    void reduce_grads() {
+        auto& api = NcclApi::get();
+        const int h = prof_begin();
+        api.GroupStart();
+        int64_t soff = 0;
+        for (auto& t : P) {
+            for (int j = 0; j < world; ++j) {
+                uint16_t* dst = recvbuf + (int64_t)j * shard_total + soff;
+                const uint16_t* src = grads + t.off + (int64_t)j * t.pw;
+                if (j == rank) {
+                    cudaMemcpyAsync(recvbuf + (int64_t)rank * shard_total + soff, src, t.pw * 2,
+                                    cudaMemcpyDeviceToDevice, st);
+                } else {
+                    api.Send(src, (size_t)t.pw, ncclBfloat16, j, comm, st);
+                    api.Recv(dst, (size_t)t.pw, ncclBfloat16, j, comm, st);
+                }
+            }
+            soff += t.pw;
+        }
+        ncclResult_t r = api.GroupEnd();
+        if (r != ncclSuccess) throw QtError(3, std::string("NCCL grad exchange: ") + api.GetErrorString(r));
+        ordered_sum_kernel<<<grid_for(shard_total), 256, 0, st>>>(recvbuf, world, shard_total, gshard);
+        QT_CHECK_CUDA(cudaGetLastError());
+        prof_end(h, 9, 2.0 * shard_total * (world - 1) * 2);
+    }
+
+    void grad_sumsq() {
+        const void* g = world > 1 ? (const void*)gshard : (const void*)grads;
+        QT_CHECK_K(qtk_grad_sumsq(g, world > 1, segs_dev, nsegs, norm_blocks, norm_partials, norm_scratch, ssq_dev, st));
+        if (world > 1) {
+            auto& api = NcclApi::get();
+            ncclResult_t r = api.AllReduce(ssq_dev, ssq_dev, 1, ncclFloat64, ncclSum, comm, st);
+            if (r != ncclSuccess) throw QtError(3, std::string("NCCL norm allreduce: ") + api.GetErrorString(r));
+        }
+    }
+
+    // AdamW on this rank's shard + all-gather of the updated bf16 params (optim.cpp:112-176)
+    void adamw(const float* grad_scale_dev) {
+        const int64_t step = step_count + 1;
+        const float bc1 = 1.0f - std::pow(hyper.beta1, static_cast<float>(step));
+        const float bc2 = 1.0f - std::pow(hyper.beta2, static_cast<float>(step));
+        const void* g = world > 1 ? (const void*)gshard : (const void*)grads;
+        const int64_t total = world > 1 ? shard_total : p_total;
+        int h = prof_begin();
+        QT_CHECK_K(qtk_adamw_dev(params, m32, v32, m16, v16, g, world > 1, segs_dev, nsegs, total, hyper.lr, hyper.beta1,
+                                 hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev, seed, step,
+                                 plan.bf16_moments, err_dev, nullptr, st));
+        prof_end(h, 10, (double)total * (plan.bf16_moments ? 14.0 : 22.0));
+        if (world > 1) {
+            auto& api = NcclApi::get();
+            h = prof_begin();
+            api.GroupStart();
+            for (auto& t : P)
+                api.AllGather(params + t.off + (int64_t)rank * t.pw, params + t.off, (size_t)t.pw, ncclBfloat16, comm,
+                              st);
+            ncclResult_t r = api.GroupEnd();
+            if (r != ncclSuccess) throw QtError(3, std::string("NCCL param all-gather: ") + api.GetErrorString(r));
+            prof_end(h, 9, 2.0 * shard_total * (world - 1));
+        }
+        step_count += 1;
+    }
+
+    // ---------------- one trainer step (src/trainer.cpp:64-110) ----------------
+    void train_step(const int32_t* tokens, int64_t tokens_per_mb, int64_t batch, int64_t step, float max_norm) {
+        const int GA = plan.ga_steps;
+        build_step_context();
+        QT_CHECK_CUDA(cudaMemsetAsync(grads, 0, p_total * 2, st));
+        for (int ga = 0; ga < GA; ++ga) {
+            forward(tokens + (int64_t)ga * tokens_per_mb, tokens_per_mb, batch, true);
+            QT_CHECK_CUDA(cudaMemcpyAsync(loss_dev + 1 + ga, loss_dev, 4, cudaMemcpyDeviceToDevice, st));
+            backward((uint64_t)step * GA + ga);
+        }
+        if (world > 1) reduce_grads();
+        grad_sumsq();
+        const float mean_scale = 1.0f / (static_cast<float>(GA) * world);
+        finalize_scale_kernel<<<1, 1, 0, st>>>(ssq_dev, mean_scale, max_norm, gscale_dev, norm_dev);
+        QT_CHECK_CUDA(cudaGetLastError());
+        step_count = step;
+        adamw(gscale_dev);
+    }
+
+    // non-finite diagnostics (model.cpp:125-129, trainer.cpp:113-115)
+    void check_errors(bool after_forward) {
+        int err = 0;
+        QT_CHECK_CUDA(cudaMemcpyAsync(&err, err_dev, 4, cudaMemcpyDeviceToHost, st));
+        std::vector<uint32_t> am((size_t)L * 4);
+        uint32_t fa = 0;
+        float loss = 0;
+        QT_CHECK_CUDA(cudaMemcpyAsync(am.data(), act_amax, L * 16, cudaMemcpyDeviceToHost, st));
+        QT_CHECK_CUDA(cudaMemcpyAsync(&fa, fin_amax, 4, cudaMemcpyDeviceToHost, st));
+        QT_CHECK_CUDA(cudaMemcpyAsync(&loss, loss_dev, 4, cudaMemcpyDeviceToHost, st));
+        QT_CHECK_CUDA(cudaStreamSynchronize(st));
+        if (err == 2) {
+            cudaMemsetAsync(err_dev, 0, 4, st);
+            throw QtError(2, "model_forward: token id out of range");
+        }
+        if (after_forward) {
+            static const char* names[4] = {"rmsnorm1", "attention", "rmsnorm2", "swiglu"};
+            for (int l = 0; l < L; ++l)
+                for (int s = 0; s < 4; ++s)
+                    if (am[l * 4 + s] >= 0x7F800000u)
+                        throw QtError(3, std::string("non-finite value at ") + names[s] + " (layer " +
+                                             std::to_string(l) + ")");
+            if (fa >= 0x7F800000u) throw QtError(3, "non-finite value at final rmsnorm");
+            if (!std::isfinite(loss)) throw QtError(3, "non-finite value at cross entropy");
+        }
+        if (err == 3) {
+            cudaMemsetAsync(err_dev, 0, 4, st);
+            throw QtError(3, "adamw_step: non-finite gradient");
+        }
+    }
+};
+
+}  // namespace qtb
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace qtb;
+
+struct qt_session {
+    std::unique_ptr<Session> s;
+};
+
+template <typename F>
+static int guard(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const QtError& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return 3;
+    }
+}
+
+extern "C" {
+
+const char* qt_last_error(void) { return g_last_error.c_str(); }
+
+int qt_nccl_unique_id(void* out128) {
+    return guard([&] {
+        auto& api = NcclApi::get();
+        if (!api.ok) throw QtError(3, "NCCL not loadable");
+        ncclUniqueId id;
+        ncclResult_t r = api.GetUniqueId(&id);
+        if (r != ncclSuccess) throw QtError(3, api.GetErrorString(r));
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+int qt_session_create(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan, const QtAdamW* hyper,
+                      uint64_t seed, int rank, int world, const void* nccl_id, int device, qt_session** out) {
+    *out = nullptr;
+    return guard([&] {
+        auto* h = new qt_session();
+        try {
+            h->s = std::make_unique<Session>(*cfg, *prec, *plan, *hyper, seed, rank, world, nccl_id, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+void qt_session_destroy(qt_session* s) { delete s; }
+
+void* qt_session_stream(qt_session* s) { return (void*)s->s->st; }
+size_t qt_session_bytes(qt_session* s) { return s->s->arena_bytes; }
+
+int qt_num_params(qt_session* s) { return (int)s->s->P.size(); }
+
+int qt_param_info(qt_session* s, int i, const char** name, int64_t* numel) {
+    return guard([&] {
+        if (i < 0 || i >= (int)s->s->P.size()) throw QtError(2, "param index out of range");
+        *name = s->s->P[i].name.c_str();
+        *numel = s->s->P[i].numel;
+    });
+}
+
+int qt_param_upload(qt_session* h, int i, const float* host) {
+    return guard([&] {
+        Session& s = *h->s;
+        const ParamT& t = s.P.at(i);
+        QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, host, t.numel * 4, cudaMemcpyHostToDevice, s.st));
+        f32_to_bf16_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.scratch_f32, s.params + t.off, t.numel);
+        QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+    });
+}
+
+static void download_bf16(Session& s, const uint16_t* src, int64_t n, float* host) {
+    bf16_to_f32_kernel<<<grid_for(n), 256, 0, s.st>>>(src, s.scratch_f32, n);
+    QT_CHECK_CUDA(cudaMemcpyAsync(host, s.scratch_f32, n * 4, cudaMemcpyDeviceToHost, s.st));
+    QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+}
+
+int qt_param_download(qt_session* h, int i, float* host) {
+    return guard([&] {
+        Session& s = *h->s;
+        const ParamT& t = s.P.at(i);
+        download_bf16(s, s.params + t.off, t.numel, host);
+    });
+}
+
+int qt_grad_download(qt_session* h, int i, float* host) {
+    return guard([&] {
+        Session& s = *h->s;
+        const ParamT& t = s.P.at(i);
+        download_bf16(s, s.grads + t.off, t.numel, host);
+    });
+}
+
+// f32 moments of this rank's slice of tensor i (world == 1: the whole tensor)
+int qt_moments_download(qt_session* h, int i, float* m, float* v) {
+    return guard([&] {
+        Session& s = *h->s;
+        if (s.plan.bf16_moments) throw QtError(1, "bf16 moments: not supported by this accessor");
+        const ParamT& t = s.P.at(i);
+        std::vector<SegH> segs(s.nsegs);
+        QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDeviceToHost));
+        const SegH& sg = segs[i];
+        const int64_t off = s.world > 1 ? sg.off : t.off;
+        QT_CHECK_CUDA(cudaMemcpy(m, s.m32 + off, sg.n * 4, cudaMemcpyDeviceToHost));
+        QT_CHECK_CUDA(cudaMemcpy(v, s.v32 + off, sg.n * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+int qt_moments_upload(qt_session* h, int i, const float* m, const float* v, int64_t step_count) {
+    return guard([&] {
+        Session& s = *h->s;
+        if (s.plan.bf16_moments || s.world > 1) throw QtError(1, "moments upload: world == 1, f32 moments only");
+        const ParamT& t = s.P.at(i);
+        QT_CHECK_CUDA(cudaMemcpy(s.m32 + t.off, m, t.numel * 4, cudaMemcpyHostToDevice));
+        QT_CHECK_CUDA(cudaMemcpy(s.v32 + t.off, v, t.numel * 4, cudaMemcpyHostToDevice));
+        s.step_count = step_count;
+    });
+}
+
+// init_params (src/model.cpp:67-86) on device
+int qt_init_params(qt_session* h, uint64_t seed) {
+    return guard([&] {
+        Session& s = *h->s;
+        const float std_ = 1.0f / std::sqrt(static_cast<float>(s.d));
+        for (auto& t : s.P) {
+            const bool gamma = t.shape.size() == 1;
+            if (gamma)
+                fill_bf16_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.params + t.off, t.numel, 1.0f);
+            else
+                init_normal_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.params + t.off, t.numel, std_, seed, t.s_init);
+        }
+        QT_CHECK_CUDA(cudaGetLastError());
+        QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+    });
+}
+
+int qt_build_step_context(qt_session* h) {
+    return guard([&] { h->s->build_step_context(); });
+}
+
+int qt_forward(qt_session* h, const int32_t* tokens_dev, int64_t n_tokens, int64_t batch, int with_grads,
+               float* loss_host) {
+    return guard([&] {
+        Session& s = *h->s;
+        s.forward(tokens_dev, n_tokens, batch, with_grads != 0);
+        if (loss_host) {
+            s.check_errors(true);
+            QT_CHECK_CUDA(cudaMemcpy(loss_host, s.loss_dev, 4, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int qt_backward(qt_session* h, uint64_t micro_step) {
+    return guard([&] { h->s->backward(micro_step); });
+}
+
+int qt_zero_grads(qt_session* h) {
+    return guard([&] { QT_CHECK_CUDA(cudaMemsetAsync(h->s->grads, 0, h->s->p_total * 2, h->s->st)); });
+}
+
+int qt_grad_norm(qt_session* h, double* norm_host) {
+    return guard([&] {
+        Session& s = *h->s;
+        if (s.world > 1) s.reduce_grads();
+        s.grad_sumsq();
+        double ssq = 0;
+        QT_CHECK_CUDA(cudaMemcpyAsync(&ssq, s.ssq_dev, 8, cudaMemcpyDeviceToHost, s.st));
+        QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+        *norm_host = std::sqrt(ssq);
+    });
+}
+
+// adamw_step(st, params, grads, grad_scale) (src/optim.cpp:153-164); sharded when world > 1
+int qt_adamw_step(qt_session* h, float grad_scale) {
+    return guard([&] {
+        Session& s = *h->s;
+        set_scale_kernel<<<1, 1, 0, s.st>>>(s.gscale_dev, grad_scale);
+        s.adamw(s.gscale_dev);
+        s.check_errors(false);
+    });
+}
+
+// full trainer step; tokens_dev holds ga_steps micro-batches of batch*(seq+1) ids
+int qt_train_step(qt_session* h, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch, int64_t step,
+                  float max_grad_norm, float* loss_host, float* norm_host) {
+    return guard([&] {
+        Session& s = *h->s;
+        s.train_step(tokens_dev, tokens_per_mb, batch, step, max_grad_norm);
+        if (loss_host || norm_host) {
+            s.check_errors(true);
+            std::vector<float> l(s.plan.ga_steps);
+            double nrm = 0;
+            QT_CHECK_CUDA(cudaMemcpyAsync(l.data(), s.loss_dev + 1, 4 * l.size(), cudaMemcpyDeviceToHost, s.st));
+            QT_CHECK_CUDA(cudaMemcpyAsync(&nrm, s.norm_dev, 8, cudaMemcpyDeviceToHost, s.st));
+            QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+            double sum = 0;
+            for (float x : l) sum += x;
+            if (loss_host) *loss_host = (float)(sum / s.plan.ga_steps);  // per-rank mean; callers average over ranks
+            if (norm_host) *norm_host = (float)nrm;
+        }
+    });
+}
+
+// staging copy for the end-to-end path: host tokens -> the session's token buffer
+int qt_upload_tokens(qt_session* h, const int32_t* host, int64_t n, int32_t** dev_out) {
+    return guard([&] {
+        Session& s = *h->s;
+        const int64_t cap = (int64_t)s.plan.ga_steps * s.plan.micro_batch * (s.T + 1);
+        if (n > cap) throw QtError(1, "too many tokens for the session's token buffer");
+        QT_CHECK_CUDA(cudaMemcpyAsync(s.tok_buf, host, n * 4, cudaMemcpyHostToDevice, s.st));
+        *dev_out = s.tok_buf;
+    });
+}
+
+int qt_sync(qt_session* h) {
+    return guard([&] { QT_CHECK_CUDA(cudaStreamSynchronize(h->s->st)); });
+}
+
+// absmax statistics {N1, ATT, N2, H} per layer (ForwardStats, model.hpp:148-151)
+int qt_forward_stats(qt_session* h, float* out) {
+    return guard([&] {
+        Session& s = *h->s;
+        QT_CHECK_CUDA(cudaMemcpy(out, s.act_amax, s.L * 16, cudaMemcpyDeviceToHost));
+    });
+}
+
+// raw bytes of a saved site of the last forward: dtype 0 = bf16, 1 = fp8 codes, 2 = f32
+int qt_saved_raw(qt_session* h, int layer, const char* site, void* host, int64_t* bytes, int* dtype) {
+    return guard([&] {
+        Session& s = *h->s;
+        const std::string n(site);
+        const int64_t M = s.curM;
+        const void* src = nullptr;
+        int64_t nb = 0;
+        int dt = 0;
+        if (layer < 0 || layer > s.L) throw QtError(2, "layer out of range");
+        LayerBufs& b = s.lb[layer];
+        if (n == "r_in") { src = b.r_in; nb = M * s.d * 2; }
+        else if (n == "normed_final") { src = s.normed_final; nb = M * s.d * 2; }
+        else if (n == "dlogits") { src = s.dlogits; nb = M * s.V * 2; }
+        else if (n == "dlogits_lo") { src = s.dlogits_lo; nb = M * s.V * 2; }
+        else if (n == "d_hidden") { src = s.d_hidden; nb = M * s.d * 2; }
+        else if (n == "logits") { src = s.logits; nb = M * s.V * 4; dt = 2; }
+        else if (layer == s.L) throw QtError(1, "only r_in exists for layer L (r_final)");
+        else if (n == "n1c") { src = b.n1c; nb = M * s.d; dt = 1; }
+        else if (n == "qkv") { src = b.qkv; nb = M * s.q * 2; }
+        else if (n == "att") { src = b.att; nb = M * s.d * 2; }
+        else if (n == "attc") { src = b.attc; nb = M * s.d; dt = 1; }
+        else if (n == "r_mid") { src = b.r_mid; nb = M * s.d * 2; }
+        else if (n == "n2c") { src = b.n2c; nb = M * s.d; dt = 1; }
+        else if (n == "gate_up") { src = b.gu; nb = M * s.F * 2; }
+        else if (n == "hc") { src = b.hc; nb = M * s.Hh; dt = 1; }
+        else if (n == "lse") { src = b.lse; nb = (int64_t)s.curB * s.H * s.curT * 4; dt = 2; }
+        else throw QtError(1, "unknown site " + n);
+        *bytes = nb;
+        *dtype = dt;
+        if (host) QT_CHECK_CUDA(cudaMemcpy(host, src, nb, cudaMemcpyDeviceToHost));
+    });
+}
+
+// device scalars: which = 0 act scales (L*4), 1 weight scales (L*4), 2 grad scales (L*4), 3 weight amax (L*4)
+int qt_scales(qt_session* h, int which, float* out) {
+    return guard([&] {
+        Session& s = *h->s;
+        const void* src = which == 0 ? (void*)s.act_scale : which == 1 ? (void*)s.w_scale
+                        : which == 2 ? (void*)s.g_scale : (void*)s.w_amax;
+        QT_CHECK_CUDA(cudaMemcpy(out, src, s.L * 16, cudaMemcpyDeviceToHost));
+    });
+}
+
+int qt_weight_codes(qt_session* h, int layer, int which, uint8_t* host) {
+    return guard([&] {
+        Session& s = *h->s;
+        const int64_t n[4] = {(int64_t)s.q * s.d, (int64_t)s.d * s.d, (int64_t)s.F * s.d, (int64_t)s.d * s.Hh};
+        QT_CHECK_CUDA(cudaMemcpy(host, s.wcodes[layer * 4 + which], n[which], cudaMemcpyDeviceToHost));
+    });
+}
+
+int qt_set_profile(qt_session* h, int on) {
+    return guard([&] {
+        Session& s = *h->s;
+        s.prof_on = on != 0;
+        s.prof.clear();
+        s.ev_used = 0;
+    });
+}
+
+// per-category totals since qt_set_profile: ms[ncat], launches[ncat], work[ncat] (flops or bytes)
+int qt_profile_read(qt_session* h, int ncat, double* ms, int64_t* launches, double* work) {
+    return guard([&] {
+        Session& s = *h->s;
+        QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+        for (int c = 0; c < ncat; ++c) {
+            ms[c] = 0;
+            launches[c] = 0;
+            work[c] = 0;
+        }
+        for (auto& r : s.prof) {
+            if (r.cat < 0 || r.cat >= ncat) continue;
+            float t = 0;
+            cudaEventElapsedTime(&t, r.a, r.b);
+            ms[r.cat] += t;
+            launches[r.cat] += 1;
+            work[r.cat] += r.work;
+        }
+    });
+}
+
+// host-side ZeRO-1 layout (src/comms.cpp:69-73), exported for the gloo tests
+int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_worker) {
+    if (workers < 1) return 1;
+    const int64_t unit = 256 * (int64_t)workers;
+    *padded = ceil_div(numel, unit) * unit;
+    *per_worker = *padded / workers;
+    return 0;
+}
+
+uint64_t qt_fnv1a64(const char* s) { return fnv1a64(s); }
+
+}  // extern "C"

@@ -71,7 +71,8 @@ def quantize_transpose(x: torch.Tensor, kind: int, slot: torch.Tensor, with_rowm
 def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool = False, b_mn: bool = False,
          a_fmt: int = E4M3, b_fmt: int = E4M3, a_scale: torch.Tensor | None = None,
          b_scale: torch.Tensor | None = None, epi: int = EPI_BF16, out: torch.Tensor | None = None,
-         res: torch.Tensor | None = None, sr: tuple[int, int, int] = (0, 0, 0), bn: int = 0) -> torch.Tensor:
+         res: torch.Tensor | None = None, sr: tuple[int, int, int] = (0, 0, 0), bn: int = 0,
+         a2: torch.Tensor | None = None) -> torch.Tensor:
     """D[m,n] = sum_k A[m,k] B[n,k].  A stored [M][K] (a_mn=False) or [K][M]
     (a_mn=True); likewise B.  uint8 operands are FP8 codes, bf16 operands BF16."""
     _need_cuda(a, b)
@@ -89,5 +90,81 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
     g.res, g.ldr = _p(res), (res.stride(0) if res is not None else 0)
     g.sr_seed, g.sr_stream, g.sr_base = sr
     g.bn = bn
+    g.a2 = _p(a2)
     _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
     return out
+
+
+def ce_softmax(logits: torch.Tensor, targets: torch.Tensor, inv_n: float, with_grads: bool = True):
+    """Per-row CE loss and dlogits (bf16 hi, bf16 lo) from f32 logits."""
+    _need_cuda(logits, targets)
+    rows, V = logits.shape
+    loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    hi = torch.empty((rows, V), dtype=torch.bfloat16, device=logits.device) if with_grads else None
+    lo = torch.empty((rows, V), dtype=torch.bfloat16, device=logits.device) if with_grads else None
+    rc = _lib.lib().qtk_ce_softmax(_p(logits), logits.stride(0), rows, V, _p(targets), inv_n, _p(hi), _p(lo), V,
+                                   _p(loss), _s())
+    _lib.check(rc, "qtk_ce_softmax")
+    return loss, hi, lo
+
+
+def rmsnorm_fwd(x, res, gamma, eps=1e-6, with_absmax=True):
+    rows, d = res.shape
+    nr = torch.empty_like(res) if x is not None else None
+    normed = torch.empty_like(res)
+    slot = torch.zeros(1, dtype=torch.int32, device=res.device) if with_absmax else None
+    rc = _lib.lib().qtk_rmsnorm_fwd(_p(x), _p(res), _p(gamma), rows, d, eps, _p(nr), _p(normed), None, _p(slot), _s())
+    _lib.check(rc, "qtk_rmsnorm_fwd")
+    return nr, normed, slot
+
+
+def rmsnorm_bwd(nr, gamma, dy, d_extra=None, eps=1e-6):
+    rows, d = nr.shape
+    nblk = _lib.lib().qtk_rmsnorm_bwd_partials(rows, d)
+    part = torch.empty((nblk, d), dtype=torch.float32, device=nr.device)
+    dg = torch.empty(d, dtype=torch.float32, device=nr.device)
+    din = torch.empty_like(nr)
+    slot = torch.zeros(1, dtype=torch.int32, device=nr.device)
+    rc = _lib.lib().qtk_rmsnorm_bwd(_p(nr), _p(gamma), rows, d, eps, _p(dy), _p(d_extra), _p(din), _p(part), _p(dg),
+                                    _p(slot), _s())
+    _lib.check(rc, "qtk_rmsnorm_bwd")
+    return din, dg, slot
+
+
+def swiglu_fwd(gu):
+    rows, two_h = gu.shape
+    h = torch.empty((rows, two_h // 2), dtype=torch.bfloat16, device=gu.device)
+    slot = torch.zeros(1, dtype=torch.int32, device=gu.device)
+    _lib.check(_lib.lib().qtk_swiglu_fwd(_p(gu), rows, two_h // 2, _p(h), _p(slot), _s()), "qtk_swiglu_fwd")
+    return h, slot
+
+
+def swiglu_bwd(gu, dh):
+    rows, two_h = gu.shape
+    out = torch.empty_like(gu)
+    slot = torch.zeros(1, dtype=torch.int32, device=gu.device)
+    _lib.check(_lib.lib().qtk_swiglu_bwd(_p(gu), _p(dh), rows, two_h // 2, _p(out), _p(slot), _s()), "qtk_swiglu_bwd")
+    return out, slot
+
+
+def attn_fwd(qkv, B, T, H, Hkv, hd):
+    rows, qkv_dim = qkv.shape
+    d = H * hd
+    out = torch.empty((rows, d), dtype=torch.bfloat16, device=qkv.device)
+    out32 = torch.empty((rows, d), dtype=torch.float32, device=qkv.device)
+    lse = torch.empty((B, H, T), dtype=torch.float32, device=qkv.device)
+    slot = torch.zeros(1, dtype=torch.int32, device=qkv.device)
+    rc = _lib.lib().qtk_attn_fwd(_p(qkv), B, T, H, Hkv, hd, qkv_dim, _p(out), d, _p(out32), _p(lse), _p(slot), _s())
+    _lib.check(rc, "qtk_attn_fwd")
+    return out, out32, lse, slot
+
+
+def attn_bwd(qkv, out32, dout, lse, B, T, H, Hkv, hd):
+    rows, qkv_dim = qkv.shape
+    d = H * hd
+    Dv = torch.empty((B, H, T), dtype=torch.float32, device=qkv.device)
+    dqkv = torch.zeros_like(qkv)
+    rc = _lib.lib().qtk_attn_bwd(_p(qkv), _p(out32), _p(dout), d, _p(lse), _p(Dv), B, T, H, Hkv, hd, qkv_dim,
+                                 _p(dqkv), _s())
+    _lib.check(rc, "qtk_attn_bwd")
+    return dqkv
