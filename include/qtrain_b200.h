@@ -222,6 +222,8 @@ int qt_set_profile(qt_session* s, int on);
 int qt_profile_read(qt_session* s, int ncat, double* ms, int64_t* launches, double* work);
 int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_worker);
 uint64_t qt_fnv1a64(const char* s);
+int qt_count_step_kernels(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch,
+                          int64_t* kernels, int64_t* other_nodes);
 
 #ifdef __cplusplus
 }

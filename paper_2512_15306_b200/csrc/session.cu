@@ -1237,4 +1237,40 @@ int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_wo
 
 uint64_t qt_fnv1a64(const char* s) { return fnv1a64(s); }
 
+// Exact count of this library's kernel launches in one trainer step: the
+// step is captured into a CUDA graph (not executed) and its kernel nodes are
+// counted.  Collective nodes (NCCL) are counted separately.
+int qt_count_step_kernels(qt_session* h, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch,
+                          int64_t* kernels, int64_t* other_nodes) {
+    return guard([&] {
+        Session& s = *h->s;
+        const int64_t saved_step = s.step_count;
+        cudaGraph_t g = nullptr;
+        QT_CHECK_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeRelaxed));
+        try {
+            s.train_step(tokens_dev, tokens_per_mb, batch, saved_step, s.hyper.max_grad_norm);
+        } catch (...) {
+            cudaStreamEndCapture(s.st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        QT_CHECK_CUDA(cudaStreamEndCapture(s.st, &g));
+        s.step_count = saved_step;
+        size_t n = 0;
+        QT_CHECK_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+        std::vector<cudaGraphNode_t> nodes(n);
+        QT_CHECK_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+        int64_t k = 0, o = 0;
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            cudaGraphNodeGetType(nd, &t);
+            if (t == cudaGraphNodeTypeKernel) ++k;
+            else if (t != cudaGraphNodeTypeEmpty) ++o;
+        }
+        cudaGraphDestroy(g);
+        *kernels = k;
+        *other_nodes = o;
+    });
+}
+
 }  // extern "C"

@@ -160,6 +160,7 @@ _SIGS = {
     "qt_profile_read": (_ci, [_vp, _ci, _vp, _vp, _vp]),
     "qt_shard_layout": (_ci, [_i64, _ci, C.POINTER(_i64), C.POINTER(_i64)]),
     "qt_fnv1a64": (_u64, [C.c_char_p]),
+    "qt_count_step_kernels": (_ci, [_vp, _vp, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)]),
 }
 _bound = False
 
@@ -374,6 +375,12 @@ class Session:
         out = np.empty(n, np.uint8)
         _chk(lib().qt_weight_codes(self.h, layer, which, out.ctypes.data))
         return out
+
+    def count_step_kernels(self, tokens, batch: int) -> tuple[int, int]:
+        ptr, n = self._tokens_dev(tokens)
+        k, o = _i64(), _i64()
+        _chk(lib().qt_count_step_kernels(self.h, ptr, n // self.plan.ga_steps, batch, C.byref(k), C.byref(o)))
+        return k.value, o.value
 
     def set_profile(self, on: bool) -> None:
         _chk(lib().qt_set_profile(self.h, int(on)))
