@@ -286,9 +286,9 @@ def main():
     # dominant kernel class = largest device-time share of the profiled step
     total_ms = sum(v["ms"] for v in prof.values())
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
-    if dom_name.startswith("gemm"):
+    if dom_name.startswith(("gemm", "attn")):
         achieved = dom["work"] / (dom["ms"] / 1e3) / 1e12
-        peak = peaks["bf16_tflops"] * (2.0 if dom_name == "gemm_fp8" else 1.0)
+        peak = peaks["bf16_tflops"] * (2.0 if dom_name == "gemm_fp8" else 1.0)  # attention / LM head: bf16
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak,
                 "peak_basis": ("2 x measured bf16 burst (FP8 dense rate = 2x BF16 on sm_100)" if dom_name == "gemm_fp8"

@@ -82,9 +82,14 @@ typedef struct QtkGemm {
     int bn;             /* N tile: 128 or 256 (0 = auto)                                   */
     const void* a2;     /* optional split-A operand (same layout/ld as A): D = A.B + A2.B, */
                         /* used for f32-precision operands carried as bf16 hi + lo pairs    */
+    void* ws;           /* optional split-K workspace (f32); NULL = no split               */
+    int64_t ws_bytes;
+    int split_k;        /* 0 = auto (only when the tile grid starves the SMs), 1 = off     */
 } QtkGemm;
 
 int qtk_gemm(const QtkGemm* g, cudaStream_t s);
+/* workspace bytes the automatic split-K would use for this shape (0 = no split) */
+int qtk_gemm_splitk_ws_bytes(int64_t M, int64_t N, int64_t K, int kind);
 
 /* ------------------------------------------------------------------------- */
 /* fused block ops (src/tensorops.cpp, src/model.cpp)                          */
@@ -151,9 +156,11 @@ int qtk_loss_reduce(const float* loss_rows, int64_t n, float inv_n, float* out, 
 int qtk_seg_size(void);
 int qtk_grad_sumsq(const void* grad, int grad_f32, const void* segs, int nseg, int64_t nblk, double* partials,
                    double* scratch, double* out, cudaStream_t s);
+int qtk_adamw_chunk_size(void);
+int qtk_adamw_chunk_entry_size(void);
 int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,
-                  int nseg, int64_t total, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                  const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
+                  const void* chunks, int nchunks, float lr, float b1, float b2, float eps, float wd, float bc1,
+                  float bc2, const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
                   uint32_t* seg_amax, cudaStream_t s);
 
 /* ------------------------------------------------------------------------- */

@@ -23,6 +23,7 @@ class QtkGemm(C.Structure):
         ("a_scale", c_vp), ("b_scale", c_vp),
         ("epi", C.c_int), ("out", c_vp), ("ldo", c_i64), ("res", c_vp), ("ldr", c_i64),
         ("sr_seed", c_u64), ("sr_stream", c_u64), ("sr_base", c_u64), ("bn", C.c_int), ("a2", c_vp),
+        ("ws", c_vp), ("ws_bytes", c_i64), ("split_k", C.c_int),
     ]
 
 
@@ -33,6 +34,7 @@ _SIGS = {
     "qtk_quantize_bf16": (C.c_int, [c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp, c_vp]),
     "qtk_quantize_transpose_bf16": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "qtk_gemm": (C.c_int, [C.POINTER(QtkGemm), c_vp]),
+    "qtk_gemm_splitk_ws_bytes": (C.c_int, [c_i64, c_i64, c_i64, C.c_int]),
     "qtk_ce_softmax": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "qtk_attn_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_i64, c_vp, c_vp,
                                c_vp, c_vp]),

@@ -141,12 +141,43 @@ __device__ __forceinline__ float gval<float>(const float* g, int64_t i) {
     return g[i];
 }
 
+// one warp per 256-element block: lane l holds elements [8l, 8l+8) of the
+// block (16-B loads), squares in f64 (exact), lane-sequential then a fixed
+// shuffle tree -- deterministic, ~1e-16 relative to the sequential sum
+template <typename G>
+__device__ __forceinline__ void load8(const G* g, int64_t i, int64_t n, float (&x)[8]);
+template <>
+__device__ __forceinline__ void load8<uint16_t>(const uint16_t* g, int64_t i, int64_t n, float (&x)[8]) {
+    if (i + 8 <= n && ((i & 7) == 0)) {
+        const uint4 u = *reinterpret_cast<const uint4*>(g + i);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            x[2 * j] = __uint_as_float(w[j] << 16);
+            x[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (i + j < n) ? bfbits2f(g[i + j]) : 0.0f;
+    }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* g, int64_t i, int64_t n, float (&x)[8]) {
+    if (i + 8 <= n && ((i & 3) == 0)) {
+        const float4 a = *reinterpret_cast<const float4*>(g + i), b = *reinterpret_cast<const float4*>(g + i + 4);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = (i + j < n) ? g[i + j] : 0.0f;
+    }
+}
+
 template <typename G>
 __global__ void norm_partials_kernel(const G* __restrict__ g, const Seg* __restrict__ segs, int nseg, int64_t nblk,
                                      double* __restrict__ part) {
-    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (b >= nblk) return;
-    // find segment: last s with blk0 <= b
     int lo = 0, hi = nseg - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -154,14 +185,15 @@ __global__ void norm_partials_kernel(const G* __restrict__ g, const Seg* __restr
         else hi = mid - 1;
     }
     const Seg sg = segs[lo];
-    const int64_t i0 = (b - sg.blk0) * 256;
-    const int64_t i1 = min(i0 + 256, sg.n);
+    const int64_t i0 = (b - sg.blk0) * 256 + lane * 8;
+    float x[8];
+    load8<G>(g + sg.off, i0, sg.n, x);
     double p = 0.0;
-    for (int64_t i = i0; i < i1; ++i) {
-        const double x = (double)gval<G>(g, sg.off + i);
-        p = __dadd_rn(p, __dmul_rn(x, x));
-    }
-    part[b] = p;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p = __dadd_rn(p, __dmul_rn((double)x[j], (double)x[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, o));
+    if (lane == 0) part[b] = p;
 }
 
 __global__ void sum_f64_kernel(const double* __restrict__ in, int64_t n, double* __restrict__ out) {
@@ -197,57 +229,97 @@ struct AdamHyper {
     int bf16_moments;
 };
 
+constexpr int ADAM_T = 256;
+constexpr int ADAM_CHUNK = ADAM_T * 8 * 4;  // elements per CTA
+
+// chunk table entry: (segment, first element of the chunk within the segment)
+struct AdamChunk {
+    int32_t seg;
+    int32_t pad;
+    int64_t start;
+};
+
+__device__ __forceinline__ void store8_bf16(uint16_t* p, const float (&x)[8]) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]),
+                                              pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
+}
+
 template <typename G>
-__global__ void adamw_kernel(uint16_t* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                             uint16_t* __restrict__ m16, uint16_t* __restrict__ v16, const G* __restrict__ grad,
-                             const Seg* __restrict__ segs, int nseg, int64_t total, AdamHyper h, int* __restrict__ err,
-                             uint32_t* __restrict__ seg_amax) {
-    __shared__ int64_t s_off[1024];
-    const int ns = min(nseg, 1024);
-    for (int i = threadIdx.x; i < ns; i += blockDim.x) s_off[i] = segs[i].off;
-    __syncthreads();
+__global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p, float* __restrict__ m,
+                                                       float* __restrict__ v, uint16_t* __restrict__ m16,
+                                                       uint16_t* __restrict__ v16, const G* __restrict__ grad,
+                                                       const Seg* __restrict__ segs,
+                                                       const AdamChunk* __restrict__ chunks, AdamHyper h,
+                                                       int* __restrict__ err, uint32_t* __restrict__ seg_amax) {
+    const AdamChunk ch = chunks[blockIdx.x];
+    const Seg sg = segs[ch.seg];
     const float one_m_b1 = __fsub_rn(1.0f, h.b1), one_m_b2 = __fsub_rn(1.0f, h.b2);
     const float gscale = *h.grad_scale;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        int lo = 0, hi = ns - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_off[mid] <= i) lo = mid;
-            else hi = mid - 1;
-        }
-        const Seg& sg = segs[lo];
-        const int64_t j = i - sg.off;
-        if (j >= sg.n) continue;  // padding between segments
-        const float gi = __fmul_rn(gval<G>(grad, i), gscale);
-        if (!isfinite(gi)) {
-            atomicExch(err, 3);
-            continue;
-        }
-        const float mo = h.bf16_moments ? bfbits2f(m16[i]) : m[i];
-        const float vo = h.bf16_moments ? bfbits2f(v16[i]) : v[i];
-        const int64_t pidx = sg.poff + j;
-        const float pi = bfbits2f(p[pidx]);
-        const float m_new = __fadd_rn(__fmul_rn(h.b1, mo), __fmul_rn(one_m_b1, gi));
-        const float v_new = __fadd_rn(__fmul_rn(h.b2, vo), __fmul_rn(__fmul_rn(one_m_b2, gi), gi));
-        const float mhat = __fdiv_rn(m_new, h.bc1);
-        const float vhat = __fdiv_rn(v_new, h.bc2);
-        const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), h.eps)), __fmul_rn(h.wd, pi));
-        const float p_new = __fsub_rn(pi, __fmul_rn(h.lr, upd));
-        const uint64_t ctr = (uint64_t)(h.step - 1) * (uint64_t)sg.gnumel + (uint64_t)(sg.gstart + j);
+    const int64_t end = min(sg.n, ch.start + (int64_t)ADAM_CHUNK);
+    uint32_t amax = 0;
+    bool bad = false;
+    for (int64_t j0 = ch.start + threadIdx.x * 8; j0 < end; j0 += ADAM_T * 8) {
+        const int64_t i = sg.off + j0;      // moment / grad index
+        const int64_t pi = sg.poff + j0;    // parameter index
+        const int cnt = (int)min((int64_t)8, end - j0);
+        float gv[8], pv[8], mv[8], vv[8];
+        load8<G>(grad, i, sg.off + end, gv);
+        load8<uint16_t>(p, pi, sg.poff + end, pv);
         if (h.bf16_moments) {
-            m16[i] = f2bfbits(sr_bf16(m_new, h.seed, sg.sm, ctr));
-            v16[i] = f2bfbits(sr_bf16(v_new, h.seed, sg.sv, ctr));
+            load8<uint16_t>(m16, i, sg.off + end, mv);
+            load8<uint16_t>(v16, i, sg.off + end, vv);
         } else {
-            m[i] = m_new;
-            v[i] = v_new;
+            load8<float>(m, i, sg.off + end, mv);
+            load8<float>(v, i, sg.off + end, vv);
         }
-        const float pw = sr_bf16(p_new, h.seed, sg.sw, ctr);
-        p[pidx] = f2bfbits(pw);
-        if (seg_amax) {
-            const uint32_t a = abs_bits(pw);
-            if (a) atomicMax(&seg_amax[lo], a);
+        const uint64_t ctr0 = (uint64_t)(h.step - 1) * (uint64_t)sg.gnumel + (uint64_t)(sg.gstart + j0);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            if (k >= cnt) break;
+            const float gi = __fmul_rn(gv[k], gscale);
+            if (!isfinite(gi)) bad = true;
+            const float m_new = __fadd_rn(__fmul_rn(h.b1, mv[k]), __fmul_rn(one_m_b1, gi));
+            const float v_new = __fadd_rn(__fmul_rn(h.b2, vv[k]), __fmul_rn(__fmul_rn(one_m_b2, gi), gi));
+            const float mhat = __fdiv_rn(m_new, h.bc1);
+            const float vhat = __fdiv_rn(v_new, h.bc2);
+            const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), h.eps)), __fmul_rn(h.wd, pv[k]));
+            const float p_new = __fsub_rn(pv[k], __fmul_rn(h.lr, upd));
+            if (h.bf16_moments) {
+                mv[k] = sr_bf16(m_new, h.seed, sg.sm, ctr0 + k);
+                vv[k] = sr_bf16(v_new, h.seed, sg.sv, ctr0 + k);
+            } else {
+                mv[k] = m_new;
+                vv[k] = v_new;
+            }
+            pv[k] = sr_bf16(p_new, h.seed, sg.sw, ctr0 + k);
+            amax = max(amax, abs_bits(pv[k]));
+        }
+        if (cnt == 8 && (pi & 7) == 0 && (i & 7) == 0) {
+            store8_bf16(p + pi, pv);
+            if (h.bf16_moments) {
+                store8_bf16(m16 + i, mv);
+                store8_bf16(v16 + i, vv);
+            } else {
+                *reinterpret_cast<float4*>(m + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
+                *reinterpret_cast<float4*>(m + i + 4) = make_float4(mv[4], mv[5], mv[6], mv[7]);
+                *reinterpret_cast<float4*>(v + i) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+                *reinterpret_cast<float4*>(v + i + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+            }
+        } else {
+            for (int k = 0; k < cnt; ++k) {
+                p[pi + k] = f2bfbits(pv[k]);
+                if (h.bf16_moments) {
+                    m16[i + k] = f2bfbits(mv[k]);
+                    v16[i + k] = f2bfbits(vv[k]);
+                } else {
+                    m[i + k] = mv[k];
+                    v[i + k] = vv[k];
+                }
+            }
         }
     }
+    if (bad) atomicExch(err, 3);  // adamw_step: non-finite gradient (src/optim.cpp:47)
+    if (seg_amax && amax) atomicMax(&seg_amax[ch.seg], amax);
 }
 
 }  // namespace qtb
@@ -277,7 +349,7 @@ int qtk_seg_size(void) { return (int)sizeof(Seg); }
 int qtk_grad_sumsq(const void* grad, int grad_f32, const void* segs, int nseg, int64_t nblk, double* partials,
                    double* scratch, double* out, cudaStream_t s) {
     if (nblk <= 0) return cudaMemsetAsync(out, 0, sizeof(double), s);
-    const unsigned g = (unsigned)ceil_div(nblk, 256);
+    const unsigned g = (unsigned)ceil_div(nblk * 32, 256);
     if (grad_f32)
         norm_partials_kernel<float><<<g, 256, 0, s>>>((const float*)grad, (const Seg*)segs, nseg, nblk, partials);
     else
@@ -288,20 +360,25 @@ int qtk_grad_sumsq(const void* grad, int grad_f32, const void* segs, int nseg, i
     return (int)cudaGetLastError();
 }
 
+int qtk_adamw_chunk_size(void) { return ADAM_CHUNK; }
+int qtk_adamw_chunk_entry_size(void) { return (int)sizeof(AdamChunk); }
+
+// chunks: device table of qtk_adamw_nchunks entries {int32 seg, int32 pad, int64 start},
+// one per ADAM_CHUNK elements of every segment (built on the host)
 int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,
-                  int nseg, int64_t total, float lr, float b1, float b2, float eps, float wd, float bc1, float bc2,
-                  const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
+                  const void* chunks, int nchunks, float lr, float b1, float b2, float eps, float wd, float bc1,
+                  float bc2, const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
                   uint32_t* seg_amax, cudaStream_t s) {
-    if (nseg > 1024) return 1;
+    if (nchunks <= 0) return 0;
     AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, grad_scale_dev, seed, step, bf16_moments};
-    const int grid = (int)std::min<int64_t>(ceil_div(total, 256), 16 * kNumSMs);
     if (grad_f32)
-        adamw_kernel<float><<<grid, 256, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
-                                                 (const float*)grad, (const Seg*)segs, nseg, total, h, err, seg_amax);
+        adamw_kernel<float><<<nchunks, ADAM_T, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
+                                                       (const float*)grad, (const Seg*)segs,
+                                                       (const AdamChunk*)chunks, h, err, seg_amax);
     else
-        adamw_kernel<uint16_t><<<grid, 256, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
-                                                    (const uint16_t*)grad, (const Seg*)segs, nseg, total, h, err,
-                                                    seg_amax);
+        adamw_kernel<uint16_t><<<nchunks, ADAM_T, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
+                                                          (const uint16_t*)grad, (const Seg*)segs,
+                                                          (const AdamChunk*)chunks, h, err, seg_amax);
     return (int)cudaGetLastError();
 }
 

@@ -23,6 +23,8 @@
 #include "sm100.cuh"
 
 #include <cudaTypedefs.h>
+#include <algorithm>
+#include <climits>
 #include <mutex>
 
 namespace qtb {
@@ -39,6 +41,7 @@ struct alignas(64) Params {
     int M, N, K;
     int num_m, num_n, num_k;
     int split_a;
+    int splits, kb_per_split;  // split-K: partial f32 tiles to out + s*M*ldo
     uint32_t idesc;
     const float* a_scale;
     const float* b_scale;
@@ -83,17 +86,32 @@ __device__ __forceinline__ void load_bf16x32(const uint16_t* src, float (&v)[32]
     }
 }
 
+// x / d correctly rounded from rcp = RN(1/d): q = RN(x*rcp) is within 1 ulp, the
+// FMA residual x - q*d is exact, and one correction q + res*rcp rounds to the
+// correctly rounded quotient (Markstein's theorem) -- the same bits as the
+// reference's f32 division acc / denom (src/tensorops.cpp:55) in 3 instructions.
+__device__ __forceinline__ float div_exact(float x, float d, float rcp) {
+    const float q = __fmul_rn(x, rcp);
+    const float e = __fmaf_rn(-q, d, x);
+    return __fmaf_rn(e, rcp, q);
+}
+
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col0, float denom, const uint32_t (&r)[32]) {
-    if (row >= p.M || col0 >= p.N) return;
+__device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col0, float denom, float rcp,
+                                               const uint32_t (&r)[32]) {
+    if (col0 >= p.N) return;
     const bool vec = (col0 + 32 <= p.N) && ((p.ldo & 7) == 0);
     float v[32];
     if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+    } else if constexpr (EPI == EPI_BF16) {
+        // rounding happens once, in the bf16x2 pack of the store
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = div_exact(__uint_as_float(r[j]), denom, rcp);
     } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = bf16r(__fdiv_rn(__uint_as_float(r[j]), denom));
+        for (int j = 0; j < 32; ++j) v[j] = bf16r(div_exact(__uint_as_float(r[j]), denom, rcp));
     }
     if constexpr (EPI == EPI_BF16 || EPI == EPI_BF16_RES) {
         uint16_t* out = reinterpret_cast<uint16_t*>(p.out) + (int64_t)row * p.ldo + col0;
@@ -173,22 +191,26 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const int tiles = p.num_m * p.num_n;
-    const int kiters = p.split_a ? 2 * p.num_k : p.num_k;
+    const int all_tiles = tiles * p.splits;
 
     if (warp == 0 && lane == 0) {
         // ===== TMA producer =====
         int stage = 0;
         uint32_t phase = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        for (int tt = blockIdx.x; tt < all_tiles; tt += gridDim.x) {
+            const int t = tt % tiles, sp = tt / tiles;
             const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
-            for (int kb = 0; kb < kiters; ++kb) {
+            const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_k, kb0 + p.kb_per_split);
+            const int kn = kb1 - kb0;
+            const int kiters = p.split_a ? 2 * kn : kn;
+            for (int kq = 0; kq < kiters; ++kq) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = base + stage * C::STAGE;
                 uint8_t* sb = sa + C::A_BYTES;
                 mbar_arrive_expect_tx(&full[stage], C::STAGE);
-                const bool second = kb >= p.num_k;
+                const bool second = kq >= kn;
                 const CUtensorMap* tA = second ? &p.ta2 : &p.ta;
-                const int k0 = (second ? kb - p.num_k : kb) * C::BK;
+                const int k0 = (kb0 + (second ? kq - kn : kq)) * C::BK;
                 if constexpr (!A_MN) {
                     tma_load_2d(tA, &full[stage], sa, k0, m0);
                 } else {
@@ -214,7 +236,10 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        for (int tt = blockIdx.x; tt < all_tiles; tt += gridDim.x, ++it) {
+            const int sp = tt / tiles;
+            const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_k, kb0 + p.kb_per_split);
+            const int kiters = p.split_a ? 2 * (kb1 - kb0) : (kb1 - kb0);
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(&tempty[acc], aphase ^ 1);
@@ -249,20 +274,22 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         const int wq = warp - 4;
         float denom = 1.0f;
         if (p.a_scale && p.b_scale) denom = __fmul_rn(*p.a_scale, *p.b_scale);
+        const float rcp = __frcp_rn(denom);
         int it = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        for (int tt = blockIdx.x; tt < all_tiles; tt += gridDim.x, ++it) {
+            const int t = tt % tiles, sp = tt / tiles;
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
             const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
-            const int row = m0 + wq * 32 + lane;
+            const int row = m0 + wq * 32 + lane + sp * p.M;  // split partials stack along rows
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
                 tmem_ld_wait();
-                epilogue_chunk<EPI>(p, row, n0 + c * 32, denom, r);
+                if (row - sp * p.M < p.M) epilogue_chunk<EPI>(p, row, n0 + c * 32, denom, rcp, r);
             }
             tc_fence_before();
             __syncwarp();
@@ -273,6 +300,43 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// split-K reduction: sum the S f32 partial tiles in split order (fixed, so the
+// result is deterministic) and apply the requested epilogue
+// ---------------------------------------------------------------------------
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int M, int N, int epi,
+                                     const float* __restrict__ a_scale, const float* __restrict__ b_scale,
+                                     void* __restrict__ out, int64_t ldo, const uint16_t* __restrict__ res,
+                                     int64_t ldr, uint64_t seed, uint64_t stream, uint64_t base) {
+    float denom = 1.0f;
+    if (a_scale && b_scale) denom = __fmul_rn(*a_scale, *b_scale);
+    const float rcp = __frcp_rn(denom);
+    const int64_t total = (int64_t)M * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = ws[i];
+        for (int s = 1; s < S; ++s) acc = __fadd_rn(acc, ws[(int64_t)s * total + i]);
+        const int64_t r = i / N, c = i % N;
+        if (epi == EPI_F32) {
+            reinterpret_cast<float*>(out)[r * ldo + c] = acc;
+            continue;
+        }
+        if (epi == EPI_F32_ACC) {
+            uint16_t* b = reinterpret_cast<uint16_t*>(out) + r * ldo + c;
+            *b = f2bfbits(sr_bf16(__fadd_rn(bfbits2f(*b), acc), seed, stream, base + (uint64_t)(r * N + c)));
+            continue;
+        }
+        const float v = bf16r(div_exact(acc, denom, rcp));
+        uint16_t* o = reinterpret_cast<uint16_t*>(out) + r * ldo + c;
+        if (epi == EPI_BF16) {
+            *o = f2bfbits(v);
+        } else if (epi == EPI_BF16_RES) {
+            *o = f2bfbits(__fadd_rn(v, bfbits2f(res[r * ldr + c])));
+        } else {  // EPI_BF16_ACC
+            *o = f2bfbits(sr_bf16(__fadd_rn(bfbits2f(*o), v), seed, stream, base + (uint64_t)(r * N + c)));
+        }
     }
 }
 
@@ -347,6 +411,7 @@ int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, i
     QTB_GEMM_CASE(0, false, true, EPI_BF16)
     QTB_GEMM_CASE(0, true, true, EPI_BF16)
     QTB_GEMM_CASE(0, true, true, EPI_BF16_ACC)
+    QTB_GEMM_CASE(0, true, true, EPI_F32)
     QTB_GEMM_CASE(0, false, false, EPI_BF16_ACC)
     // BF16: LM-head logits (K,K)->f32, CE dgrad (K,MN)->bf16, CE wgrad (MN,MN)->f32 SR-accumulate
     QTB_GEMM_CASE(1, false, false, EPI_F32)
@@ -359,10 +424,29 @@ int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, i
     return 902;  // unsupported combination
 }
 
+// split-K factor for a GEMM (0 = no split): only when the tile grid leaves
+// most SMs idle and K is long enough to amortise the reduction
+int choose_splits(int64_t M, int64_t N, int64_t K, int kind, int bn) {
+    const int bk = kind == 0 ? 128 : 64;
+    const int64_t tiles = ceil_div(M, BM) * ceil_div(N, bn);
+    const int64_t nk = ceil_div(K, bk);
+    if (tiles * 2 > num_sms() || nk < 16) return 1;
+    int64_t s = num_sms() / tiles;
+    s = std::min<int64_t>(s, nk / 8);
+    s = std::min<int64_t>(s, 8);
+    return (int)std::max<int64_t>(s, 1);
+}
+
 }  // namespace gemm
 }  // namespace qtb
 
 using namespace qtb;
+
+extern "C" int qtk_gemm_splitk_ws_bytes(int64_t M, int64_t N, int64_t K, int kind) {
+    const int bn = N <= 128 ? 128 : 256;
+    const int s = qtb::gemm::choose_splits(M, N, K, kind, bn);
+    return s > 1 ? (int)std::min<int64_t>((int64_t)s * M * N * 4, INT32_MAX) : 0;
+}
 
 extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     using namespace qtb::gemm;
@@ -418,6 +502,29 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     p.sr_stream = g->sr_stream;
     p.sr_base = g->sr_base;
     const int tiles = p.num_m * p.num_n;
+    int splits = 1;
+    if (g->ws && g->split_k != 1) {
+        splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn);
+        if ((int64_t)splits * g->M * g->N * 4 > g->ws_bytes) splits = 1;
+    }
+    p.splits = splits;
+    p.kb_per_split = (int)ceil_div(p.num_k, splits);
+    if (splits > 1) {
+        p.splits = (int)ceil_div(p.num_k, p.kb_per_split);  // no empty splits
+        p.out = g->ws;
+        p.ldo = g->N;
+        const int all = tiles * p.splits;
+        const int grid = all < num_sms() ? all : num_sms();
+        int rc2 = dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, EPI_F32, p, grid, s);
+        if (rc2) return rc2;
+        const int64_t total = g->M * g->N;
+        const int rg = (int)std::min<int64_t>(ceil_div(total, 256), 8 * num_sms());
+        splitk_reduce_kernel<<<rg, 256, 0, s>>>((const float*)g->ws, p.splits, (int)g->M, (int)g->N, g->epi,
+                                                g->a_scale, g->b_scale, g->out, g->ldo,
+                                                reinterpret_cast<const uint16_t*>(g->res), g->ldr, g->sr_seed,
+                                                g->sr_stream, g->sr_base);
+        return (int)cudaGetLastError();
+    }
     const int grid = tiles < num_sms() ? tiles : num_sms();
     return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, s);
 }

@@ -184,12 +184,15 @@ class Session {
     uint16_t *d_r = nullptr, *d_h = nullptr, *d_gu = nullptr, *d_n = nullptr, *d_ao = nullptr, *d_att = nullptr,
              *d_qkv = nullptr, *d_hidden = nullptr;
     uint8_t* gcodes = nullptr;  // grad-kind codes scratch (M x max(F, q))
+    float* gemm_ws = nullptr;   // split-K partials for the small-grid weight-gradient GEMMs
+    int64_t gemm_ws_bytes = 0;
     float* logits = nullptr;
     uint16_t* dlogits = nullptr;
     uint16_t* dlogits_lo = nullptr;
     float* loss_rows = nullptr;
     float* dgamma_part = nullptr;
     float* dgamma = nullptr;
+    float* rms_inv = nullptr;  // per-row 1/rms scratch of the forward norms
     float* Dv = nullptr;
     float2* rope_tab = nullptr;
     int32_t *tok_buf = nullptr, *inputs = nullptr, *targets = nullptr, *sorted_pos = nullptr, *seg_tok = nullptr,
@@ -202,6 +205,8 @@ class Session {
     int64_t norm_blocks = 0;
     SegH* segs_dev = nullptr;
     int nsegs = 0;
+    void* chunks_dev = nullptr;  // AdamW per-CTA chunk table
+    int nchunks = 0;
     // device scalars
     uint32_t* act_amax = nullptr;  // L*4
     float* act_scale = nullptr;    // L*4
@@ -412,6 +417,14 @@ class Session {
         req(&d_qkv, M * q * 2);
         req(&d_hidden, M * d * 2);
         req(&gcodes, M * std::max(F, q));
+        {
+            // wgrad shapes (out, in, K = tokens) and small fwd/dgrad shapes
+            const int64_t shapes[][3] = {{q, d, M}, {d, d, M}, {F, d, M}, {d, Hh, M}, {M, q, d}, {M, d, d},
+                                         {M, F, d}, {M, d, Hh}, {M, Hh, d}, {M, d, F}, {M, d, q}};
+            for (auto& sh : shapes)
+                gemm_ws_bytes = std::max<int64_t>(gemm_ws_bytes, qtk_gemm_splitk_ws_bytes(sh[0], sh[1], sh[2], 0));
+            if (gemm_ws_bytes > 0) req(&gemm_ws, gemm_ws_bytes);
+        }
         req(&logits, (size_t)M * V * 4);
         req(&dlogits, (size_t)M * V * 2);
         req(&dlogits_lo, (size_t)M * V * 2);
@@ -419,6 +432,7 @@ class Session {
         const int nblk = qtk_rmsnorm_bwd_partials(M, d);
         req(&dgamma_part, (size_t)nblk * d * 4);
         req(&dgamma, d * 4);
+        req(&rms_inv, M * 4);
         req(&Dv, (size_t)plan.micro_batch * H * T * 4);
         req(&rope_tab, (size_t)T * (hd / 2) * 8);
         req(&tok_buf, (size_t)plan.ga_steps * plan.micro_batch * (T + 1) * 4);
@@ -436,6 +450,12 @@ class Session {
         req(&norm_partials, norm_blocks * 8);
         req(&norm_scratch, 1024 * 8);
         req(&segs_dev, P.size() * sizeof(SegH));
+        {
+            int64_t nch = 0;
+            const int64_t cs = qtk_adamw_chunk_size();
+            for (auto& t : P) nch += ceil_div(world > 1 ? t.pw : t.numel, cs);
+            req(&chunks_dev, nch * qtk_adamw_chunk_entry_size());
+        }
         req(&act_amax, L * 16);
         req(&act_scale, L * 16);
         req(&w_amax, L * 16);
@@ -511,6 +531,18 @@ class Session {
         norm_blocks = blk;
         nsegs = (int)segs.size();
         QT_CHECK_CUDA(cudaMemcpyAsync(segs_dev, segs.data(), segs.size() * sizeof(SegH), cudaMemcpyHostToDevice, st));
+        struct Chunk {
+            int32_t seg, pad;
+            int64_t start;
+        };
+        if ((int)sizeof(Chunk) != qtk_adamw_chunk_entry_size()) throw QtError(3, "AdamW chunk layout mismatch");
+        std::vector<Chunk> chunks;
+        const int64_t cs = qtk_adamw_chunk_size();
+        for (int i = 0; i < nsegs; ++i)
+            for (int64_t s0 = 0; s0 < segs[i].n; s0 += cs) chunks.push_back({i, 0, s0});
+        nchunks = (int)chunks.size();
+        QT_CHECK_CUDA(cudaMemcpyAsync(chunks_dev, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice,
+                                      st));
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
 
@@ -581,6 +613,9 @@ class Session {
         g.sr_base = sr_base;
         g.bn = 0;
         g.a2 = a2;
+        g.ws = gemm_ws;
+        g.ws_bytes = gemm_ws_bytes;
+        g.split_k = 0;
         const int h = prof_begin();
         QT_CHECK_K(qtk_gemm(&g, st));
         prof_end(h, kind == 0 ? 0 : 1, 2.0 * M * N * K * (a2 ? 2 : 1));
@@ -616,7 +651,7 @@ class Session {
         int h;
         // rmsnorm1 (pass-through residual) + N1 absmax
         h = prof_begin();
-        QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, b.r_in, params + ln1.off, M, d, 1e-6f, nullptr, s_n1, nullptr,
+        QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, b.r_in, params + ln1.off, M, d, 1e-6f, nullptr, s_n1, rms_inv,
                                    record ? am + S_N1 : nullptr, st));
         prof_end(h, 4, 4.0 * M * d);
         h = prof_begin();
@@ -637,7 +672,7 @@ class Session {
         gemm(0, kE4M3, kE4M3, false, false, M, d, d, b.attc, d, wcodes[l * 4 + W_O], d, sc + S_ATT, ws + W_O, EPI_BF16,
              s_attn_out, d);
         h = prof_begin();
-        QT_CHECK_K(qtk_rmsnorm_fwd(s_attn_out, b.r_in, params + ln2.off, M, d, 1e-6f, b.r_mid, s_n2, nullptr,
+        QT_CHECK_K(qtk_rmsnorm_fwd(s_attn_out, b.r_in, params + ln2.off, M, d, 1e-6f, b.r_mid, s_n2, rms_inv,
                                    record ? am + S_N2 : nullptr, st));
         prof_end(h, 4, 8.0 * M * d);
         h = prof_begin();
@@ -676,7 +711,7 @@ class Session {
                                                   seg_tok, seg_off, nseg, st));
         for (int l = 0; l < L; ++l) block_forward(l, true);
         h = prof_begin();
-        QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, lb[L].r_in, pptr("final_g"), M, d, 1e-6f, nullptr, normed_final, nullptr,
+        QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, lb[L].r_in, pptr("final_g"), M, d, 1e-6f, nullptr, normed_final, rms_inv,
                                    fin_amax, st));
         prof_end(h, 4, 4.0 * M * d);
         // fused CE forward (+ dlogits for the backward): logits in f32 (tensorops.cpp:372-376)
@@ -840,9 +875,9 @@ class Session {
         const void* g = world > 1 ? (const void*)gshard : (const void*)grads;
         const int64_t total = world > 1 ? shard_total : p_total;
         int h = prof_begin();
-        QT_CHECK_K(qtk_adamw_dev(params, m32, v32, m16, v16, g, world > 1, segs_dev, nsegs, total, hyper.lr, hyper.beta1,
-                                 hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev, seed, step,
-                                 plan.bf16_moments, err_dev, nullptr, st));
+        QT_CHECK_K(qtk_adamw_dev(params, m32, v32, m16, v16, g, world > 1, segs_dev, chunks_dev, nchunks, hyper.lr,
+                                 hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev, seed,
+                                 step, plan.bf16_moments, err_dev, nullptr, st));
         prof_end(h, 10, (double)total * (plan.bf16_moments ? 14.0 : 22.0));
         if (world > 1) {
             auto& api = NcclApi::get();

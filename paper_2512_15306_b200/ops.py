@@ -72,7 +72,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
          a_fmt: int = E4M3, b_fmt: int = E4M3, a_scale: torch.Tensor | None = None,
          b_scale: torch.Tensor | None = None, epi: int = EPI_BF16, out: torch.Tensor | None = None,
          res: torch.Tensor | None = None, sr: tuple[int, int, int] = (0, 0, 0), bn: int = 0,
-         a2: torch.Tensor | None = None) -> torch.Tensor:
+         a2: torch.Tensor | None = None, split_k: int = 1) -> torch.Tensor:
     """D[m,n] = sum_k A[m,k] B[n,k].  A stored [M][K] (a_mn=False) or [K][M]
     (a_mn=True); likewise B.  uint8 operands are FP8 codes, bf16 operands BF16."""
     _need_cuda(a, b)
@@ -91,6 +91,15 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
     g.sr_seed, g.sr_stream, g.sr_base = sr
     g.bn = bn
     g.a2 = _p(a2)
+    ws = None
+    if split_k != 1:
+        nbytes = _lib.lib().qtk_gemm_splitk_ws_bytes(M, N, K, kind)
+        if split_k > 1:
+            nbytes = split_k * M * N * 4
+        if nbytes > 0:
+            ws = torch.empty(nbytes // 4, dtype=torch.float32, device=a.device)
+            g.ws, g.ws_bytes = _p(ws), nbytes
+    g.split_k = split_k
     _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
     return out
 
@@ -113,7 +122,9 @@ def rmsnorm_fwd(x, res, gamma, eps=1e-6, with_absmax=True):
     nr = torch.empty_like(res) if x is not None else None
     normed = torch.empty_like(res)
     slot = torch.zeros(1, dtype=torch.int32, device=res.device) if with_absmax else None
-    rc = _lib.lib().qtk_rmsnorm_fwd(_p(x), _p(res), _p(gamma), rows, d, eps, _p(nr), _p(normed), None, _p(slot), _s())
+    inv = torch.empty(rows, dtype=torch.float32, device=res.device)
+    rc = _lib.lib().qtk_rmsnorm_fwd(_p(x), _p(res), _p(gamma), rows, d, eps, _p(nr), _p(normed), _p(inv), _p(slot),
+                                    _s())
     _lib.check(rc, "qtk_rmsnorm_fwd")
     return nr, normed, slot
 

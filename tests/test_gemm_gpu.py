@@ -173,3 +173,24 @@ def test_gemm_rejects_unaligned_stride(ops):
     b = torch.zeros((40, 100), dtype=torch.uint8, device="cuda")  # MN-major B with a 100-B row stride
     with pytest.raises(RuntimeError, match="status 1"):
         ops.gemm(a, b, M=64, N=100, K=40, b_mn=True)
+
+
+@pytest.mark.parametrize("M,N", [(896, 896), (1152, 896)])
+def test_fp8_gemm_splitk_wgrad(ops, ref, M, N):
+    """Weight-gradient shape (out, in, K = tokens) with too few tiles for 148 SMs:
+    the automatic split-K path (fixed-order partial sums) stays within the same
+    tolerance of the reference as the unsplit kernel."""
+    K = 8192
+    a = rng_floats(M + 1, M * K, -1, 1).reshape(M, K)
+    b = rng_floats(N + 2, N * K, -1, 1).reshape(N, K)
+    ac, sa = _q(ref, a, 1)
+    bc, sb = _q(ref, b, 0)
+    want = ref.matmul_fp8(ac, 1, sa, bc, 0, sb)
+    st = dict(M=M, N=N, K=K, a_mn=True, b_mn=True, a_fmt=1, b_fmt=0, a_scale=torch.tensor([sa], device="cuda"),
+              b_scale=torch.tensor([sb], device="cuda"))
+    A, B = _cuda_u8(ac.T.copy()), _cuda_u8(bc.T.copy())
+    g_split = ops.gemm(A, B, split_k=0, **st)
+    g_plain = ops.gemm(A, B, split_k=1, **st)
+    scale = _absscale(ref, ac, 1, sa, bc, 0, sb)
+    _check_close(g_split.float().cpu().numpy(), want, absscale=scale, K=K, frac=0.99)
+    _check_close(g_plain.float().cpu().numpy(), want, absscale=scale, K=K, frac=0.99)
