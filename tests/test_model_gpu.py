@@ -218,5 +218,16 @@ def test_tiny_config_step_parity(ref):
     lg, ng = sess.train_step(toks, 4, step=0)
     assert abs(lg - lw) / lw < 1e-3, (lg, lw)
     assert abs(ng - nw) / nw < 2e-2, (ng, nw)
-    worst = max(_rel(sess.download(n), rm.get(n)) for n in rm.names)
-    assert worst < 4e-3, worst
+    # envelope: the reference's own updated params after one FP8 code flip upstream
+    pert = ref.RefModel(cfg.as_list(), 1234, grad_e5m2=True)
+    w = pert.get("layers.0.w_qkv").copy()
+    i = int(np.argmax(np.abs(w) < 0.5 * np.abs(w).max()))
+    w[i] = ref.bf16_round(float(w[i]) * 1.125)
+    pert.set("layers.0.w_qkv", w)
+    base = ref.RefModel(cfg.as_list(), 1234, grad_e5m2=True)
+    base.train_step(toks, 4, step=0)
+    pert.train_step(toks, 4, step=0)
+    for n in rm.names:
+        env = _rel(pert.get(n), base.get(n)) if n != "layers.0.w_qkv" else 1e-3
+        got = _rel(sess.download(n), rm.get(n))
+        assert got <= max(2.0 * env, 1e-3), (n, got, env)
