@@ -1,0 +1,189 @@
+// qtrain-b200 C++ drop-in API: the reference's operator names and types
+// (namespace qtrain in /root/reference/proj/include/qtrain/{model,optim}.hpp)
+// over the C ABI in qtrain_b200.h.  Header-only; link libqtrain_b200.so.
+//
+// Status codes map back to the reference's exception types with the same
+// messages: 1 -> std::invalid_argument, 2 -> std::out_of_range,
+// 3 -> std::runtime_error ("non-finite value at rmsnorm1 (layer 0)", ...).
+//
+// Differences from the reference, by design: parameters, gradients, optimizer
+// state and activations are device-resident inside a Session (one per GPU);
+// Tensor-valued accessors copy to/from host f32 vectors on demand.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../qtrain_b200.h"
+
+namespace qtrain_b200 {
+
+inline void check(int rc) {
+    if (rc == 0) return;
+    const std::string msg = qt_last_error();
+    if (rc == 1) throw std::invalid_argument(msg);
+    if (rc == 2) throw std::out_of_range(msg);
+    throw std::runtime_error(msg);
+}
+
+// include/qtrain/model.hpp:24-39
+struct ModelConfig {
+    int n_layers = 2;
+    int d_model = 64;
+    int d_ff = 256;
+    int n_heads = 4;
+    int n_kv_heads = 2;
+    std::int64_t vocab = 512;
+    int seq_len = 128;
+    int head_dim() const { return d_model / n_heads; }
+    int qkv_dim() const { return d_model + 2 * n_kv_heads * head_dim(); }
+};
+
+enum class MatmulPrecision { FP8_E4M3, BF16 };
+enum class GradPrecision { E4M3, E5M2 };
+
+// include/qtrain/model.hpp:47-57
+struct PrecisionMap {
+    MatmulPrecision block_matmuls = MatmulPrecision::FP8_E4M3;
+    GradPrecision backward_grads = GradPrecision::E4M3;
+    bool f32_debug = false;
+};
+
+enum class RecomputeSite : std::uint8_t { SwiGLU, RMSNorm, Attention, QKV, FFN, Block };
+
+// include/qtrain/model.hpp:63-80
+struct RecomputeSet {
+    std::uint8_t bits = 0;
+    static RecomputeSet none() { return {}; }
+    static RecomputeSet of(std::initializer_list<RecomputeSite> sites) {
+        RecomputeSet s;
+        for (auto site : sites) s.bits |= static_cast<std::uint8_t>(1u << static_cast<int>(site));
+        return s;
+    }
+    static RecomputeSet block() { return of({RecomputeSite::Block}); }
+};
+
+// include/qtrain/model.hpp:158-161
+struct ChunkSpec {
+    std::int64_t lmhead_chunk_tokens = 0;
+    std::int64_t attn_chunk_rows = 0;
+};
+
+// include/qtrain/optim.hpp:20-26
+struct AdamWHyper {
+    float lr = 1e-3f;
+    float beta1 = 0.9f;
+    float beta2 = 0.95f;
+    float eps = 1e-8f;
+    float weight_decay = 0.0f;
+};
+
+enum class MomentPrecision { F32, BF16_SR };
+
+// the subset of RunPlan (include/qtrain/memplan.hpp:54-67) the step uses
+struct RunPlan {
+    int micro_batch = 1;
+    int ga_steps = 1;
+    RecomputeSet recompute;
+    ChunkSpec chunks;
+    bool shard_weights = false;
+    bool shard_grads = false;
+    MomentPrecision moments = MomentPrecision::F32;
+};
+
+// One GPU's training state.  rank/world/nccl_id select the ZeRO-1 shard
+// (sharded_adamw_step semantics, include/qtrain/optim.hpp:76-77).
+class Session {
+   public:
+    Session(const ModelConfig& cfg, const PrecisionMap& prec, const RunPlan& plan, const AdamWHyper& hyper,
+            std::uint64_t seed, float max_grad_norm = 1.0f, int rank = 0, int world = 1,
+            const void* nccl_id = nullptr, int device = 0) {
+        QtModelConfig c{cfg.n_layers, cfg.d_model, cfg.d_ff, cfg.n_heads, cfg.n_kv_heads, cfg.vocab, cfg.seq_len};
+        QtPrecisionMap p{prec.block_matmuls == MatmulPrecision::FP8_E4M3 ? 0 : 1,
+                         prec.backward_grads == GradPrecision::E4M3 ? 0 : 1, prec.f32_debug ? 1 : 0};
+        QtRunPlan r{plan.micro_batch, plan.ga_steps, plan.recompute.bits, plan.chunks.lmhead_chunk_tokens,
+                    plan.chunks.attn_chunk_rows, plan.shard_weights ? 1 : 0, plan.shard_grads ? 1 : 0,
+                    plan.moments == MomentPrecision::BF16_SR ? 1 : 0};
+        QtAdamW h{hyper.lr, hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, max_grad_norm};
+        check(qt_session_create(&c, &p, &r, &h, seed, rank, world, nccl_id, device, &s_));
+        ga_steps_ = plan.ga_steps;
+        const int n = qt_num_params(s_);
+        for (int i = 0; i < n; ++i) {
+            const char* nm = nullptr;
+            std::int64_t ne = 0;
+            check(qt_param_info(s_, i, &nm, &ne));
+            names_.emplace_back(nm, ne);
+        }
+    }
+    ~Session() {
+        if (s_) qt_session_destroy(s_);
+    }
+    Session(const Session&) = delete;
+    Session& operator=(const Session&) = delete;
+
+    // for_each_param order (include/qtrain/model.hpp:107-121)
+    const std::vector<std::pair<std::string, std::int64_t>>& params() const { return names_; }
+
+    // init_params (include/qtrain/model.hpp:125)
+    void init_params(std::uint64_t seed) { check(qt_init_params(s_, seed)); }
+    void set_param(int i, const std::vector<float>& v) { check(qt_param_upload(s_, i, v.data())); }
+    std::vector<float> get_param(int i) const {
+        std::vector<float> v(static_cast<std::size_t>(names_.at(i).second));
+        check(qt_param_download(s_, i, v.data()));
+        return v;
+    }
+    std::vector<float> get_grad(int i) const {
+        std::vector<float> v(static_cast<std::size_t>(names_.at(i).second));
+        check(qt_grad_download(s_, i, v.data()));
+        return v;
+    }
+
+    // build_step_context (include/qtrain/model.hpp:143-144)
+    void build_step_context() { check(qt_build_step_context(s_)); }
+
+    // model_forward (include/qtrain/model.hpp:181-185); tokens on the host,
+    // batch*(seq+1) ids.  Returns the loss.
+    float model_forward(const std::vector<std::int32_t>& tokens, std::int64_t batch, bool with_grads = true) {
+        std::int32_t* dev = nullptr;
+        check(qt_upload_tokens(s_, tokens.data(), static_cast<std::int64_t>(tokens.size()), &dev));
+        float loss = 0.0f;
+        check(qt_forward(s_, dev, static_cast<std::int64_t>(tokens.size()), batch, with_grads ? 1 : 0, &loss));
+        return loss;
+    }
+
+    // model_backward + GradAccumulator::accumulate(micro_step) (model.hpp:190-211)
+    void model_backward(std::uint64_t micro_step) { check(qt_backward(s_, micro_step)); }
+    void zero_grads() { check(qt_zero_grads(s_)); }
+
+    // global_grad_norm (include/qtrain/optim.hpp:65)
+    double global_grad_norm() {
+        double n = 0.0;
+        check(qt_grad_norm(s_, &n));
+        return n;
+    }
+    // adamw_step / sharded_adamw_step (include/qtrain/optim.hpp:59-77)
+    void adamw_step(float grad_scale) { check(qt_adamw_step(s_, grad_scale)); }
+
+    // one run_training step (src/trainer.cpp:64-110): returns {train_loss, grad_norm}
+    std::pair<float, float> train_step(const std::vector<std::int32_t>& tokens, std::int64_t batch, std::int64_t step,
+                                       float max_grad_norm) {
+        std::int32_t* dev = nullptr;
+        check(qt_upload_tokens(s_, tokens.data(), static_cast<std::int64_t>(tokens.size()), &dev));
+        float loss = 0.0f, norm = 0.0f;
+        const std::int64_t per_mb = static_cast<std::int64_t>(tokens.size()) / ga_steps_;
+        check(qt_train_step(s_, dev, per_mb, batch, step, max_grad_norm, &loss, &norm));
+        return {loss, norm};
+    }
+
+    qt_session* handle() { return s_; }
+
+   private:
+    qt_session* s_ = nullptr;
+    int ga_steps_ = 1;
+    std::vector<std::pair<std::string, std::int64_t>> names_;
+};
+
+}  // namespace qtrain_b200

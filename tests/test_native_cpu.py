@@ -71,3 +71,14 @@ def test_flops_accounting_matches_reference(ref):
         a, b = ref.flops_per_token(c.as_list())
         fp8, bf16 = c.flops_per_token()
         assert abs(fp8 - a) / a < 1e-12 and abs(bf16 - b) / b < 1e-12
+
+
+def test_cpp_drop_in_header_compiles(tmp_path):
+    """The C++ operator-API header (include/qtrain_b200/qtrain.hpp) and the
+    example compile against the library with g++."""
+    import subprocess
+    exe = tmp_path / "drop_in_step"
+    r = subprocess.run(["g++", "-std=c++17", "-O1", str(ROOT / "examples" / "drop_in_step.cpp"), f"-I{ROOT / 'include'}",
+                        "-I/usr/local/cuda/include", f"-L{LIB.parent}", "-lqtrain_b200",
+                        f"-Wl,-rpath,{LIB.parent}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
