@@ -141,8 +141,13 @@ int qtk_embed_bwd(const int32_t* sorted_pos, const int32_t* seg_off, const int32
  * src/tensorops.cpp:191-303) on the (B*T, qkv_dim) RoPE'd tensor. */
 int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
                  float* out32, float* lse, uint32_t* amax, cudaStream_t s);
+/* precision mode (process-wide): fast_exp = __expf for exp(); bwd_split = P and
+ * dS carried as bf16 hi+lo in the backward MMAs (default 0, 1) */
+void qtk_attn_set_mode(int fast_exp, int bwd_split);
+/* ws: qtk_attn_bwd_ws_bytes(...) of f32 scratch for the GQA per-head dK/dV partials */
+size_t qtk_attn_bwd_ws_bytes(int B, int T, int H, int Hkv, int hd);
 int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv, int B,
-                 int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, cudaStream_t s);
+                 int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s);
 
 /* fused_cross_entropy_chunked softmax stage (src/tensorops.cpp:367-393):
  * per-row loss and dlogits from f32 logits; dlogits (f32 in the reference) is

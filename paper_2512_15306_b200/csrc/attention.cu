@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
+
 namespace qtb { namespace attn { __device__ __forceinline__ uint32_t sm100_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); } } }
 
 namespace qtb {
@@ -118,7 +120,13 @@ __device__ __forceinline__ void ld_b_kn(uint32_t (&b)[4], uint32_t s, int k0, in
 // ===========================================================================
 // forward: grid (ceil(T/64), H, B), 4 warps x 16 query rows
 // ===========================================================================
-template <int HD>
+template <bool FAST>
+__device__ __forceinline__ float att_exp(float x) {
+    if constexpr (FAST) return __expf(x);
+    else return expf(x);
+}
+
+template <int HD, bool FAST = false>
 __global__ void __launch_bounds__(128) fwd_kernel(const uint16_t* __restrict__ qkv, int T, int H, int Hkv, int qkv_dim,
                                                   float inv_sqrt_d, uint16_t* __restrict__ out, int64_t ldo,
                                                   float* __restrict__ out32, float* __restrict__ lse,
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(128) fwd_kernel(const uint16_t* __restrict__ q
         float corr[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            corr[r] = (m_r[r] == -INFINITY) ? 0.0f : expf(m_r[r] - mx[r]);
+            corr[r] = (m_r[r] == -INFINITY) ? 0.0f : att_exp<FAST>(m_r[r] - mx[r]);
             m_r[r] = mx[r];
             l_r[r] *= corr[r];
         }
@@ -222,7 +230,7 @@ __global__ void __launch_bounds__(128) fwd_kernel(const uint16_t* __restrict__ q
         for (int i = 0; i < BK / 8; ++i) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                const float p = (s[i][e] == -INFINITY) ? 0.0f : expf(s[i][e] - m_r[e >> 1]);
+                const float p = (s[i][e] == -INFINITY) ? 0.0f : att_exp<FAST>(s[i][e] - m_r[e >> 1]);
                 s[i][e] = p;
                 l_r[e >> 1] += p;
             }
@@ -310,31 +318,55 @@ __global__ void bwd_dot_kernel(const uint16_t* __restrict__ dout, const float* _
 // dK/dV: grid (ceil(T/64), Hkv, B); each warp owns 16 kv rows; loops over the
 // GQA group's heads and every query block at or after the kv block
 // ===========================================================================
-template <int HD, int BQ>
+template <int HD, int BQ, bool SPLIT = true, bool FAST = false>
 __global__ void __launch_bounds__(128) bwd_dkdv_kernel(const uint16_t* __restrict__ qkv, const uint16_t* __restrict__ dout,
                                                        int64_t ldd, const float* __restrict__ lse,
                                                        const float* __restrict__ Dv, int T, int H, int Hkv,
-                                                       int qkv_dim, float inv_sqrt_d, uint16_t* __restrict__ dqkv) {
+                                                       int qkv_dim, float inv_sqrt_d, uint16_t* __restrict__ dqkv,
+                                                       float* __restrict__ ws) {
+    // grid (kv blocks, query heads, batch): one CTA per (kv block, query head);
+    // with GQA (group > 1) the per-head f32 dK/dV go to ws and a second kernel
+    // adds the group's heads in ascending order (deterministic)
     constexpr int BKV = 64;
+    constexpr int TILE = BQ * HD * 2;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sK = sm100_smem(smem);
     const uint32_t sV = sK + BKV * HD * 2;
-    const uint32_t sQ = sV + BKV * HD * 2;
-    const uint32_t sO = sQ + BQ * HD * 2;  // dO tile
-    float* sL = reinterpret_cast<float*>(smem + (2 * BKV + 2 * BQ) * HD * 2);
-    float* sD = sL + BQ;
-    const int kb = blockIdx.x, kvh = blockIdx.y, b = blockIdx.z;
+    const uint32_t sQ0 = sV + BKV * HD * 2;        // [2][Q, dO] double buffer
+    const uint32_t sLD0 = sQ0 + 4 * TILE;          // [2][L(BQ), D(BQ)] floats
+    float* sLDf = reinterpret_cast<float*>(smem + (sLD0 - sK));
+    const int kb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int d = H * HD;
     const int group = H / Hkv;
+    const int kvh = h / group;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, c4 = lane & 3;
     const int64_t rowbase = (int64_t)b * T;
     const int kvvalid = min(BKV, T - kb * BKV);
     const uint16_t* gk = qkv + (rowbase + kb * BKV) * qkv_dim + d + kvh * HD;
     const uint16_t* gv = qkv + (rowbase + kb * BKV) * qkv_dim + d + Hkv * HD + kvh * HD;
+    const float* gL = lse + ((int64_t)b * H + h) * T;
+    const float* gD = Dv + ((int64_t)b * H + h) * T;
     load_tile<HD, BKV, 128>(sK, gk, qkv_dim, kvvalid);
     load_tile<HD, BKV, 128>(sV, gv, qkv_dim, kvvalid);
-    cp_commit();
+
+    const int q_first = (kb * BKV) / BQ;
+    const int nqb = (T + BQ - 1) / BQ;
+    auto issue = [&](int qi, int buf) {
+        const int qvalid = min(BQ, T - qi * BQ);
+        const uint32_t sq = sQ0 + buf * 2 * TILE;
+        load_tile<HD, BQ, 128>(sq, qkv + (rowbase + qi * BQ) * qkv_dim + h * HD, qkv_dim, qvalid);
+        load_tile<HD, BQ, 128>(sq + TILE, dout + (rowbase + qi * BQ) * ldd + h * HD, ldd, qvalid);
+        const uint32_t sld = sLD0 + buf * 2 * BQ * 4;
+        for (int i = threadIdx.x; i < 2 * (BQ / 4); i += 128) {
+            const int which = i / (BQ / 4), c = i % (BQ / 4);
+            const int q = qi * BQ + c * 4;
+            const float* src = (which ? gD : gL) + q;
+            cp_async16(sld + which * BQ * 4 + c * 16, q < T ? src : gL, q < T);
+        }
+        cp_commit();
+    };
+    issue(q_first, 0);
 
     float dk[HD / 8][4], dv[HD / 8][4];
 #pragma unroll
@@ -343,102 +375,136 @@ __global__ void __launch_bounds__(128) bwd_dkdv_kernel(const uint16_t* __restric
         for (int e = 0; e < 4; ++e) dk[i][e] = dv[i][e] = 0.0f;
     const int kv0 = kb * BKV + warp * 16 + g;  // kv positions of this thread's rows: kv0, kv0+8
 
-    const int q_first = (kb * BKV) / BQ;
-    const int nqb = (T + BQ - 1) / BQ;
-    for (int hh = 0; hh < group; ++hh) {
-        const int h = kvh * group + hh;
-        for (int qi = q_first; qi < nqb; ++qi) {
-            __syncthreads();  // previous tiles consumed
-            const int qvalid = min(BQ, T - qi * BQ);
-            load_tile<HD, BQ, 128>(sQ, qkv + (rowbase + qi * BQ) * qkv_dim + h * HD, qkv_dim, qvalid);
-            load_tile<HD, BQ, 128>(sO, dout + (rowbase + qi * BQ) * ldd + h * HD, ldd, qvalid);
-            cp_commit();
-            for (int i = threadIdx.x; i < BQ; i += 128) {
-                const int q = qi * BQ + i;
-                sL[i] = q < T ? lse[((int64_t)b * H + h) * T + q] : 0.0f;
-                sD[i] = q < T ? Dv[((int64_t)b * H + h) * T + q] : 0.0f;
-            }
+    for (int qi = q_first, it = 0; qi < nqb; ++qi, ++it) {
+        const int buf = it & 1;
+        if (qi + 1 < nqb) {
+            issue(qi + 1, buf ^ 1);
+            cp_wait<1>();
+        } else {
             cp_wait<0>();
-            __syncthreads();
-            // S^T = K Q^T  (16 kv x BQ q per warp)
-            float st[BQ / 8][4], dpt[BQ / 8][4];
+        }
+        __syncthreads();
+        const uint32_t sQ = sQ0 + buf * 2 * TILE, sO = sQ + TILE;
+        const float* sL = sLDf + buf * 2 * BQ;
+        const float* sD = sL + BQ;
+        // S^T = K Q^T and dP^T = V dO^T  (16 kv x BQ q per warp)
+        float st[BQ / 8][4], dpt[BQ / 8][4];
 #pragma unroll
-            for (int i = 0; i < BQ / 8; ++i)
+        for (int i = 0; i < BQ / 8; ++i)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) st[i][e] = dpt[i][e] = 0.0f;
+            for (int e = 0; e < 4; ++e) st[i][e] = dpt[i][e] = 0.0f;
 #pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) {
-                uint32_t ka[4], va[4];
-                ld_a<HD>(ka, sK, warp * 16, kk * 16);
-                ld_a<HD>(va, sV, warp * 16, kk * 16);
+        for (int kk = 0; kk < HD / 16; ++kk) {
+            uint32_t ka[4], va[4];
+            ld_a<HD>(ka, sK, warp * 16, kk * 16);
+            ld_a<HD>(va, sV, warp * 16, kk * 16);
 #pragma unroll
-                for (int nn = 0; nn < BQ / 16; ++nn) {
-                    uint32_t bq[4], bo[4];
-                    ld_b_nk<HD>(bq, sQ, nn * 16, kk * 16);
-                    ld_b_nk<HD>(bo, sO, nn * 16, kk * 16);
-                    mma16816(st[2 * nn], ka, bq[0], bq[1]);
-                    mma16816(st[2 * nn + 1], ka, bq[2], bq[3]);
-                    mma16816(dpt[2 * nn], va, bo[0], bo[1]);
-                    mma16816(dpt[2 * nn + 1], va, bo[2], bo[3]);
-                }
+            for (int nn = 0; nn < BQ / 16; ++nn) {
+                uint32_t bq[4], bo[4];
+                ld_b_nk<HD>(bq, sQ, nn * 16, kk * 16);
+                ld_b_nk<HD>(bo, sO, nn * 16, kk * 16);
+                mma16816(st[2 * nn], ka, bq[0], bq[1]);
+                mma16816(st[2 * nn + 1], ka, bq[2], bq[3]);
+                mma16816(dpt[2 * nn], va, bo[0], bo[1]);
+                mma16816(dpt[2 * nn + 1], va, bo[2], bo[3]);
             }
-            // P^T and dS^T (f32), then dV += P^T dO and dK += dS^T Q with both
-            // left operands split into bf16 hi + lo parts (f32-faithful products)
+        }
+        // P^T and dS^T (f32), then dV += P^T dO and dK += dS^T Q with both
+        // left operands split into bf16 hi + lo parts (f32-faithful products)
 #pragma unroll
-            for (int i = 0; i < BQ / 8; ++i) {
+        for (int i = 0; i < BQ / 8; ++i) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int kv = kv0 + (e >> 1) * 8;
-                    const int qc = i * 8 + 2 * c4 + (e & 1);
-                    const int q = qi * BQ + qc;
-                    const bool ok = (q >= kv) && (q < T) && (kv < T);
-                    const float x = st[i][e] * inv_sqrt_d;
-                    const float p = ok ? expf(x - sL[qc]) : 0.0f;
-                    st[i][e] = p;
-                    dpt[i][e] = p * (dpt[i][e] - sD[qc]) * inv_sqrt_d;
-                }
+            for (int e = 0; e < 4; ++e) {
+                const int kv = kv0 + (e >> 1) * 8;
+                const int qc = i * 8 + 2 * c4 + (e & 1);
+                const int q = qi * BQ + qc;
+                const bool ok = (q >= kv) && (q < T) && (kv < T);
+                const float x = st[i][e] * inv_sqrt_d;
+                const float p = ok ? att_exp<FAST>(x - sL[qc]) : 0.0f;
+                st[i][e] = p;
+                dpt[i][e] = p * (dpt[i][e] - sD[qc]) * inv_sqrt_d;
             }
+        }
 #pragma unroll
-            for (int kk = 0; kk < BQ / 16; ++kk) {
-                uint32_t ph[4], pl[4], dh[4], dl[4];
-                split_frag(st[2 * kk], st[2 * kk + 1], ph, pl);
-                split_frag(dpt[2 * kk], dpt[2 * kk + 1], dh, dl);
+        for (int kk = 0; kk < BQ / 16; ++kk) {
+            uint32_t ph[4], pl[4], dh[4], dl[4];
+            split_frag(st[2 * kk], st[2 * kk + 1], ph, pl);
+            split_frag(dpt[2 * kk], dpt[2 * kk + 1], dh, dl);
 #pragma unroll
-                for (int nn = 0; nn < HD / 16; ++nn) {
-                    uint32_t bo[4], bq[4];
-                    ld_b_kn<HD>(bo, sO, kk * 16, nn * 16);
-                    ld_b_kn<HD>(bq, sQ, kk * 16, nn * 16);
-                    mma16816(dv[2 * nn], ph, bo[0], bo[1]);
-                    mma16816(dv[2 * nn + 1], ph, bo[2], bo[3]);
+            for (int nn = 0; nn < HD / 16; ++nn) {
+                uint32_t bo[4], bq[4];
+                ld_b_kn<HD>(bo, sO, kk * 16, nn * 16);
+                ld_b_kn<HD>(bq, sQ, kk * 16, nn * 16);
+                mma16816(dv[2 * nn], ph, bo[0], bo[1]);
+                mma16816(dv[2 * nn + 1], ph, bo[2], bo[3]);
+                mma16816(dk[2 * nn], dh, bq[0], bq[1]);
+                mma16816(dk[2 * nn + 1], dh, bq[2], bq[3]);
+                if constexpr (SPLIT) {
                     mma16816(dv[2 * nn], pl, bo[0], bo[1]);
                     mma16816(dv[2 * nn + 1], pl, bo[2], bo[3]);
-                    mma16816(dk[2 * nn], dh, bq[0], bq[1]);
-                    mma16816(dk[2 * nn + 1], dh, bq[2], bq[3]);
                     mma16816(dk[2 * nn], dl, bq[0], bq[1]);
                     mma16816(dk[2 * nn + 1], dl, bq[2], bq[3]);
                 }
             }
         }
+        __syncthreads();  // this buffer is refilled by the prefetch two iterations on
     }
-    // write dk, dv (rounded once)
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
         const int kv = kv0 + r * 8;
         if (kv >= T) continue;
-        uint16_t* pk = dqkv + (rowbase + kv) * qkv_dim + d + kvh * HD;
-        uint16_t* pv = dqkv + (rowbase + kv) * qkv_dim + d + Hkv * HD + kvh * HD;
+        if (group == 1) {
+            uint16_t* pk = dqkv + (rowbase + kv) * qkv_dim + d + kvh * HD;
+            uint16_t* pv = dqkv + (rowbase + kv) * qkv_dim + d + Hkv * HD + kvh * HD;
 #pragma unroll
-        for (int i = 0; i < HD / 8; ++i) {
-            *reinterpret_cast<uint32_t*>(pk + i * 8 + 2 * c4) = pack_bf16(dk[i][2 * r], dk[i][2 * r + 1]);
-            *reinterpret_cast<uint32_t*>(pv + i * 8 + 2 * c4) = pack_bf16(dv[i][2 * r], dv[i][2 * r + 1]);
+            for (int i = 0; i < HD / 8; ++i) {
+                *reinterpret_cast<uint32_t*>(pk + i * 8 + 2 * c4) = pack_bf16(dk[i][2 * r], dk[i][2 * r + 1]);
+                *reinterpret_cast<uint32_t*>(pv + i * 8 + 2 * c4) = pack_bf16(dv[i][2 * r], dv[i][2 * r + 1]);
+            }
+        } else {
+            // ws layout: [2][B][H][T][HD] f32 (dk then dv)
+            const int64_t base = (((int64_t)b * H + h) * T + kv) * HD;
+            const int64_t half = (int64_t)gridDim.z * H * T * HD;
+#pragma unroll
+            for (int i = 0; i < HD / 8; ++i) {
+                *reinterpret_cast<float2*>(ws + base + i * 8 + 2 * c4) = make_float2(dk[i][2 * r], dk[i][2 * r + 1]);
+                *reinterpret_cast<float2*>(ws + half + base + i * 8 + 2 * c4) =
+                    make_float2(dv[i][2 * r], dv[i][2 * r + 1]);
+            }
         }
+    }
+}
+
+// dK/dV of a kv head = sum over its GQA group's query heads in ascending
+// order (the reference accumulates h-outer, src/tensorops.cpp:268-296), rounded once
+__global__ void dkdv_reduce_kernel(const float* __restrict__ ws, int B, int T, int H, int Hkv, int hd, int qkv_dim,
+                                   uint16_t* __restrict__ dqkv) {
+    const int group = H / Hkv;
+    const int d = H * hd;
+    const int64_t half = (int64_t)B * H * T * hd;
+    const int64_t n = (int64_t)B * Hkv * T * hd;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % hd);
+        const int64_t r = i / hd;
+        const int t = (int)(r % T);
+        const int kvh = (int)((r / T) % Hkv);
+        const int b = (int)(r / ((int64_t)T * Hkv));
+        float sk = 0.0f, sv = 0.0f;
+        for (int hh = 0; hh < group; ++hh) {
+            const int64_t o = (((int64_t)b * H + kvh * group + hh) * T + t) * hd + c;
+            sk = __fadd_rn(sk, ws[o]);
+            sv = __fadd_rn(sv, ws[half + o]);
+        }
+        const int64_t row = (int64_t)b * T + t;
+        dqkv[row * qkv_dim + d + kvh * hd + c] = f2bfbits(sk);
+        dqkv[row * qkv_dim + d + Hkv * hd + kvh * hd + c] = f2bfbits(sv);
     }
 }
 
 // ===========================================================================
 // dQ: grid (ceil(T/64), H, B); each warp owns 16 query rows
 // ===========================================================================
-template <int HD>
+template <int HD, bool SPLIT = true, bool FAST = false>
 __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict__ qkv, const uint16_t* __restrict__ dout,
                                                      int64_t ldd, const float* __restrict__ lse,
                                                      const float* __restrict__ Dv, int T, int H, int Hkv, int qkv_dim,
@@ -447,8 +513,7 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t sQ = sm100_smem(smem);
     const uint32_t sO = sQ + BQ * HD * 2;
-    const uint32_t sK = sO + BQ * HD * 2;
-    const uint32_t sV = sK + BKV * HD * 2;
+    const uint32_t sKV0 = sO + BQ * HD * 2;  // [2][K, V] double buffer
     const int qb = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int kvh = h / (H / Hkv);
     const int d = H * HD;
@@ -456,9 +521,17 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
     const int g = lane >> 2, c4 = lane & 3;
     const int64_t rowbase = (int64_t)b * T;
     const int qvalid = min(BQ, T - qb * BQ);
+    const uint16_t* gk = qkv + rowbase * qkv_dim + d + kvh * HD;
+    const uint16_t* gv = qkv + rowbase * qkv_dim + d + Hkv * HD + kvh * HD;
     load_tile<HD, BQ, 128>(sQ, qkv + (rowbase + qb * BQ) * qkv_dim + h * HD, qkv_dim, qvalid);
     load_tile<HD, BQ, 128>(sO, dout + (rowbase + qb * BQ) * ldd + h * HD, ldd, qvalid);
-    cp_commit();
+    auto issue = [&](int j, int buf) {
+        const uint32_t k_s = sKV0 + buf * 2 * BKV * HD * 2;
+        load_tile<HD, BKV, 128>(k_s, gk + (int64_t)j * BKV * qkv_dim, qkv_dim, min(BKV, T - j * BKV));
+        load_tile<HD, BKV, 128>(k_s + BKV * HD * 2, gv + (int64_t)j * BKV * qkv_dim, qkv_dim, min(BKV, T - j * BKV));
+        cp_commit();
+    };
+    issue(0, 0);  // commits Q, dO and K/V block 0 together
     const int q0 = qb * BQ + warp * 16 + g;
     float L[2], Dd[2];
 #pragma unroll
@@ -471,15 +544,16 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
 #pragma unroll
     for (int i = 0; i < HD / 8; ++i) dq[i][0] = dq[i][1] = dq[i][2] = dq[i][3] = 0.0f;
     uint32_t qf[HD / 16][4], of[HD / 16][4];
-    const uint16_t* gk = qkv + rowbase * qkv_dim + d + kvh * HD;
-    const uint16_t* gv = qkv + rowbase * qkv_dim + d + Hkv * HD + kvh * HD;
     for (int j = 0; j <= qb; ++j) {
+        const int buf = j & 1;
+        if (j + 1 <= qb) {
+            issue(j + 1, buf ^ 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
         __syncthreads();
-        load_tile<HD, BKV, 128>(sK, gk + (int64_t)j * BKV * qkv_dim, qkv_dim, min(BKV, T - j * BKV));
-        load_tile<HD, BKV, 128>(sV, gv + (int64_t)j * BKV * qkv_dim, qkv_dim, min(BKV, T - j * BKV));
-        cp_commit();
-        cp_wait<0>();
-        __syncthreads();
+        const uint32_t sK = sKV0 + buf * 2 * BKV * HD * 2, sV = sK + BKV * HD * 2;
         if (j == 0) {
 #pragma unroll
             for (int kk = 0; kk < HD / 16; ++kk) {
@@ -514,7 +588,7 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
                 const int key = j * BKV + i * 8 + 2 * c4 + (e & 1);
                 const bool ok = key <= q && key < T && q < T;
                 const float x = s[i][e] * inv_sqrt_d;
-                const float p = ok ? expf(x - L[r]) : 0.0f;
+                const float p = ok ? att_exp<FAST>(x - L[r]) : 0.0f;
                 s[i][e] = p * (dp[i][e] - Dd[r]) * inv_sqrt_d;
             }
         }
@@ -529,10 +603,13 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
                 ld_b_kn<HD>(bk, sK, kk * 16, nn * 16);
                 mma16816(dq[2 * nn], dh, bk[0], bk[1]);
                 mma16816(dq[2 * nn + 1], dh, bk[2], bk[3]);
-                mma16816(dq[2 * nn], dl, bk[0], bk[1]);
-                mma16816(dq[2 * nn + 1], dl, bk[2], bk[3]);
+                if constexpr (SPLIT) {
+                    mma16816(dq[2 * nn], dl, bk[0], bk[1]);
+                    mma16816(dq[2 * nn + 1], dl, bk[2], bk[3]);
+                }
             }
         }
+        __syncthreads();  // buffer reused by the prefetch of block j+2
     }
 #pragma unroll
     for (int r = 0; r < 2; ++r) {
@@ -551,7 +628,16 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
 using namespace qtb;
 using namespace qtb::attn;
 
+static int g_fast_exp = 0, g_bwd_split = 1;
+
 extern "C" {
+
+// precision mode of the attention kernels: fast_exp = __expf (ex2.approx) in
+// place of expf; bwd_split = carry P and dS as bf16 hi+lo in the backward
+void qtk_attn_set_mode(int fast_exp, int bwd_split) {
+    g_fast_exp = fast_exp;
+    g_bwd_split = bwd_split;
+}
 
 int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
                  float* out32, float* lse, uint32_t* amax, cudaStream_t s) {
@@ -560,8 +646,12 @@ int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_
     dim3 grid((unsigned)ceil_div(T, 64), H, B);
     if (hd == 64) {
         const int smem = (64 + 2 * 64 * 2) * 64 * 2;
-        fwd_kernel<64><<<grid, 128, smem, s>>>((const uint16_t*)qkv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)out,
-                                               ldo, out32, lse, amax);
+        if (g_fast_exp)
+            fwd_kernel<64, true><<<grid, 128, smem, s>>>((const uint16_t*)qkv, T, H, Hkv, qkv_dim, inv_sqrt_d,
+                                                         (uint16_t*)out, ldo, out32, lse, amax);
+        else
+            fwd_kernel<64><<<grid, 128, smem, s>>>((const uint16_t*)qkv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)out,
+                                                   ldo, out32, lse, amax);
     } else if (hd == 128) {
         const int smem = (64 + 2 * 64 * 2) * 128 * 2;
         cudaFuncSetAttribute(fwd_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -577,25 +667,38 @@ int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_
     return (int)cudaGetLastError();
 }
 
-// Dv scratch: B*H*T floats
+// Dv scratch: B*H*T floats; ws: 2*B*H*T*hd floats when H > Hkv (GQA partials), else unused
+size_t qtk_attn_bwd_ws_bytes(int B, int T, int H, int Hkv, int hd) {
+    return H > Hkv ? (size_t)2 * B * H * T * hd * sizeof(float) : 0;
+}
+
 int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv, int B,
-                 int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, cudaStream_t s) {
-    if (H % Hkv) return 1;
+                 int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s) {
+    if (H % Hkv || T % 4) return 1;
+    if (H > Hkv && !ws) return 1;
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     const int64_t rows = (int64_t)B * T;
     bwd_dot_kernel<<<(unsigned)ceil_div(rows * H * 32, 256), 256, 0, s>>>((const uint16_t*)dout, out32, ldo, T,
                                                                          H, hd, rows, Dv);
-    dim3 gkv((unsigned)ceil_div(T, 64), Hkv, B), gq((unsigned)ceil_div(T, 64), H, B);
-#define QTB_ATTN_BWD(HD, BQ)                                                                                      \
+    dim3 gkv((unsigned)ceil_div(T, 64), H, B), gq((unsigned)ceil_div(T, 64), H, B);
+#define QTB_ATTN_BWD_V(HD, BQ, SP, FA)                                                                           \
     {                                                                                                             \
-        const int smem_kv = (2 * 64 + 2 * BQ) * HD * 2 + 2 * BQ * 4;                                              \
-        cudaFuncSetAttribute(bwd_dkdv_kernel<HD, BQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv);      \
-        bwd_dkdv_kernel<HD, BQ><<<gkv, 128, smem_kv, s>>>((const uint16_t*)qkv, (const uint16_t*)dout, ldo, lse, Dv, \
-                                                          T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv);       \
-        const int smem_q = 4 * 64 * HD * 2;                                                                       \
-        cudaFuncSetAttribute(bwd_dq_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);             \
-        bwd_dq_kernel<HD><<<gq, 128, smem_q, s>>>((const uint16_t*)qkv, (const uint16_t*)dout, ldo, lse, Dv, T, H, \
-                                                  Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv);                     \
+        const int smem_kv = (2 * 64 + 4 * BQ) * HD * 2 + 4 * BQ * 4;                                              \
+        cudaFuncSetAttribute(bwd_dkdv_kernel<HD, BQ, SP, FA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_kv); \
+        bwd_dkdv_kernel<HD, BQ, SP, FA><<<gkv, 128, smem_kv, s>>>((const uint16_t*)qkv, (const uint16_t*)dout, ldo,  \
+                                                                  lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d,         \
+                                                                  (uint16_t*)dqkv, ws);                            \
+        const int smem_q = 6 * 64 * HD * 2;                                                                       \
+        cudaFuncSetAttribute(bwd_dq_kernel<HD, SP, FA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_q);     \
+        bwd_dq_kernel<HD, SP, FA><<<gq, 128, smem_q, s>>>((const uint16_t*)qkv, (const uint16_t*)dout, ldo, lse, Dv, \
+                                                          T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv);         \
+    }
+#define QTB_ATTN_BWD(HD, BQ)                                     \
+    {                                                            \
+        if (g_bwd_split && g_fast_exp) QTB_ATTN_BWD_V(HD, BQ, true, true)       \
+        else if (g_bwd_split) QTB_ATTN_BWD_V(HD, BQ, true, false)               \
+        else if (g_fast_exp) QTB_ATTN_BWD_V(HD, BQ, false, true)                \
+        else QTB_ATTN_BWD_V(HD, BQ, false, false)                               \
     }
     if (hd == 64)
         QTB_ATTN_BWD(64, 64)
@@ -606,6 +709,11 @@ int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t 
     else
         return 1;
 #undef QTB_ATTN_BWD
+    if (H > Hkv) {
+        const int64_t n = (int64_t)B * Hkv * T * hd;
+        dkdv_reduce_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 16 * kNumSMs), 256, 0, s>>>(
+            ws, B, T, H, Hkv, hd, qkv_dim, (uint16_t*)dqkv);
+    }
     return (int)cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <mutex>
 
 namespace qtb {
@@ -52,15 +53,18 @@ struct alignas(64) Params {
     uint64_t sr_seed, sr_stream, sr_base;
 };
 
-template <int KIND, int BN>
+// CG = CTAs per MMA (tcgen05 cta_group): 2 pairs two SMs on a 256-row tile
+// and splits the B tile between them (half the per-SM operand traffic)
+template <int KIND, int BN, int CG = 1>
 struct Cfg {
     static constexpr int ELEM = KIND == 0 ? 1 : 2;
     static constexpr int BK = 128 / ELEM;  // K elements per pipeline stage (one 128-B swizzle row)
     static constexpr int UK = 32 / ELEM;   // K per tcgen05.mma
+    static constexpr int BN_CTA = BN / CG; // B rows held by each CTA
     static constexpr int A_BYTES = BM * 128;
-    static constexpr int B_BYTES = BN * 128;
+    static constexpr int B_BYTES = BN_CTA * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
 };
@@ -156,9 +160,23 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
     }
 }
 
-template <int KIND, bool A_MN, bool B_MN, int BN, int EPI>
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa_rank0(uint32_t local) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
+    return r;
+}
+
+template <int KIND, bool A_MN, bool B_MN, int BN, int EPI, int CG>
 __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Params p) {
-    using C = Cfg<KIND, BN>;
+    using C = Cfg<KIND, BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(base + C::STAGES * C::STAGE);
@@ -168,6 +186,8 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t crank = CG == 2 ? cluster_rank() : 0;
+    const bool leader = crank == 0;
     if (warp == 0 && lane == 0) {
         tma_prefetch(&p.ta);
         tma_prefetch(&p.tb);
@@ -180,26 +200,38 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 4 * CG);
         }
         fence_barrier_init();
         fence_async_shared();
     }
-    if (warp == 2) tmem_alloc(tslot, C::TMEM_COLS);
+    if (warp == 2) {
+        if constexpr (CG == 1) {
+            tmem_alloc(tslot, C::TMEM_COLS);
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                         "r"(C::TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
+    }
     tc_fence_before();
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tslot;
     const int tiles = p.num_m * p.num_n;
     const int all_tiles = tiles * p.splits;
+    const int cid = blockIdx.x / CG, ncl = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
-        // ===== TMA producer =====
+        // ===== TMA producer (both CTAs of a pair load their halves) =====
         int stage = 0;
         uint32_t phase = 0;
-        for (int tt = blockIdx.x; tt < all_tiles; tt += gridDim.x) {
+        for (int tt = cid; tt < all_tiles; tt += ncl) {
             const int t = tt % tiles, sp = tt / tiles;
-            const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+            const int m0 = (t % p.num_m) * BM * CG + (int)crank * BM;
+            const int n0 = (t / p.num_m) * BN + (int)crank * C::BN_CTA;
             const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_k, kb0 + p.kb_per_split);
             const int kn = kb1 - kb0;
             const int kiters = p.split_a ? 2 * kn : kn;
@@ -207,23 +239,42 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = base + stage * C::STAGE;
                 uint8_t* sb = sa + C::A_BYTES;
-                mbar_arrive_expect_tx(&full[stage], C::STAGE);
+                uint32_t bar = smem_u32(&full[stage]);
+                if constexpr (CG == 2) {
+                    bar = mapa_rank0(bar);
+                    if (leader)
+                        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[stage])),
+                                     "r"(C::STAGE * CG)
+                                     : "memory");
+                } else {
+                    mbar_arrive_expect_tx(&full[stage], C::STAGE);
+                }
                 const bool second = kq >= kn;
                 const CUtensorMap* tA = second ? &p.ta2 : &p.ta;
                 const int k0 = (kb0 + (second ? kq - kn : kq)) * C::BK;
+                auto load = [&](const CUtensorMap* m, void* dst, int c0, int c1) {
+                    if constexpr (CG == 2)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+                            "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+                            "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1)
+                            : "memory");
+                    else
+                        tma_load_2d(m, &full[stage], dst, c0, c1);
+                };
                 if constexpr (!A_MN) {
-                    tma_load_2d(tA, &full[stage], sa, k0, m0);
+                    load(tA, sa, k0, m0);
                 } else {
 #pragma unroll
                     for (int i = 0; i < BM * C::ELEM / 128; ++i)
-                        tma_load_2d(tA, &full[stage], sa + i * C::BK * 128, m0 + i * (128 / C::ELEM), k0);
+                        load(tA, sa + i * C::BK * 128, m0 + i * (128 / C::ELEM), k0);
                 }
                 if constexpr (!B_MN) {
-                    tma_load_2d(&p.tb, &full[stage], sb, k0, n0);
+                    load(&p.tb, sb, k0, n0);
                 } else {
 #pragma unroll
-                    for (int i = 0; i < BN * C::ELEM / 128; ++i)
-                        tma_load_2d(&p.tb, &full[stage], sb + i * C::BK * 128, n0 + i * (128 / C::ELEM), k0);
+                    for (int i = 0; i < C::BN_CTA * C::ELEM / 128; ++i)
+                        load(&p.tb, sb + i * C::BK * 128, n0 + i * (128 / C::ELEM), k0);
                 }
                 if (++stage == C::STAGES) {
                     stage = 0;
@@ -231,12 +282,12 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 }
             }
         }
-    } else if (warp == 1 && lane == 0) {
-        // ===== MMA issuer (single thread) =====
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ===== MMA issuer (single thread of the leader CTA) =====
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
-        for (int tt = blockIdx.x; tt < all_tiles; tt += gridDim.x, ++it) {
+        for (int tt = cid; tt < all_tiles; tt += ncl, ++it) {
             const int sp = tt / tiles;
             const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_k, kb0 + p.kb_per_split);
             const int kiters = p.split_a ? 2 * (kb1 - kb0) : (kb1 - kb0);
@@ -256,18 +307,46 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                                              : make_sdesc_sw128(sa + kk * 32, 16, 1024);
                     const uint64_t bd = B_MN ? make_sdesc_sw128(sb + kk * C::UK * 128, C::BK * 128, 1024)
                                              : make_sdesc_sw128(sb + kk * 32, 16, 1024);
-                    if constexpr (KIND == 0)
-                        mma_f8(d_tmem, ad, bd, p.idesc, (kb | kk) != 0);
-                    else
-                        mma_bf16(d_tmem, ad, bd, p.idesc, (kb | kk) != 0);
+                    const uint32_t accum = (kb | kk) != 0;
+                    if constexpr (CG == 1) {
+                        if constexpr (KIND == 0) mma_f8(d_tmem, ad, bd, p.idesc, accum);
+                        else mma_bf16(d_tmem, ad, bd, p.idesc, accum);
+                    } else {
+                        if constexpr (KIND == 0)
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+                                "l"(ad), "l"(bd), "r"(p.idesc), "r"(accum)
+                                : "memory");
+                        else
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+                                "l"(ad), "l"(bd), "r"(p.idesc), "r"(accum)
+                                : "memory");
+                    }
                 }
-                tc_commit(&empty[stage]);
+                if constexpr (CG == 1)
+                    tc_commit(&empty[stage]);
+                else
+                    asm volatile(
+                        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+                        "[%0], %1;" ::"r"(smem_u32(&empty[stage])),
+                        "h"((uint16_t)3)
+                        : "memory");
                 if (++stage == C::STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            tc_commit(&tfull[acc]);
+            if constexpr (CG == 1)
+                tc_commit(&tfull[acc]);
+            else
+                asm volatile(
+                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+                    "[%0], %1;" ::"r"(smem_u32(&tfull[acc])),
+                    "h"((uint16_t)3)
+                    : "memory");
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> rounding -> HBM =====
@@ -276,13 +355,13 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         if (p.a_scale && p.b_scale) denom = __fmul_rn(*p.a_scale, *p.b_scale);
         const float rcp = __frcp_rn(denom);
         int it = 0;
-        for (int tt = blockIdx.x; tt < all_tiles; tt += gridDim.x, ++it) {
+        for (int tt = cid; tt < all_tiles; tt += ncl, ++it) {
             const int t = tt % tiles, sp = tt / tiles;
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
-            const int m0 = (t % p.num_m) * BM, n0 = (t / p.num_m) * BN;
+            const int m0 = (t % p.num_m) * BM * CG + (int)crank * BM, n0 = (t / p.num_m) * BN;
             const int row = m0 + wq * 32 + lane + sp * p.M;  // split partials stack along rows
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
@@ -293,13 +372,25 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 1) {
+                    mbar_arrive(&tempty[acc]);
+                } else {
+                    const uint32_t rb = mapa_rank0(smem_u32(&tempty[acc]));
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
+                }
+            }
         }
     }
     __syncthreads();
+    if constexpr (CG == 2) cluster_sync_all();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc(tmem, C::TMEM_COLS);
+        if constexpr (CG == 1)
+            tmem_dealloc(tmem, C::TMEM_COLS);
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -374,18 +465,46 @@ int make_tmap(CUtensorMap* m, const void* ptr, int elem, uint64_t inner, uint64_
 
 using KernelFn = void (*)(Params);
 
-template <int KIND, bool A_MN, bool B_MN, int BN, int EPI>
-int launch(const Params& p, int grid, cudaStream_t s) {
-    using C = Cfg<KIND, BN>;
-    auto k = gemm_kernel<KIND, A_MN, B_MN, BN, EPI>;
+template <int KIND, bool A_MN, bool B_MN, int BN, int EPI, int CG>
+int launch_cg(const Params& p, int grid, cudaStream_t s) {
+    using C = Cfg<KIND, BN, CG>;
+    // an MN-major operand tile must span whole 128-B swizzle atoms per CTA
+    if constexpr (B_MN && (C::BN_CTA * C::ELEM) % 128 != 0) {
+        return 903;
+    } else {
+    auto k = gemm_kernel<KIND, A_MN, B_MN, BN, EPI, CG>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return (int)e;
         attr_set = true;
     }
-    k<<<grid, 256, C::SMEM, s>>>(p);
+    if constexpr (CG == 1) {
+        k<<<grid, 256, C::SMEM, s>>>(p);
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CG;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k, p);
+        if (e != cudaSuccess) return (int)e;
+    }
     return (int)cudaGetLastError();
+    }
+}
+
+template <int KIND, bool A_MN, bool B_MN, int BN, int EPI>
+int launch(const Params& p, int grid, int cg, cudaStream_t s) {
+    return cg == 2 ? launch_cg<KIND, A_MN, B_MN, BN, EPI, 2>(p, grid, s)
+                   : launch_cg<KIND, A_MN, B_MN, BN, EPI, 1>(p, grid, s);
 }
 
 int num_sms() {
@@ -401,10 +520,10 @@ int num_sms() {
 
 #define QTB_GEMM_CASE(KIND, AMN, BMN, EPI)                                                            \
     if (kind == KIND && a_mn == AMN && b_mn == BMN && epi == EPI)                                     \
-        return bn == 256 ? launch<KIND, AMN, BMN, 256, EPI>(p, grid, s)                               \
-                         : launch<KIND, AMN, BMN, 128, EPI>(p, grid, s);
+        return bn == 256 ? launch<KIND, AMN, BMN, 256, EPI>(p, grid, cg, s)                           \
+                         : launch<KIND, AMN, BMN, 128, EPI>(p, grid, cg, s);
 
-int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, int grid, cudaStream_t s) {
+int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, int grid, int cg, cudaStream_t s) {
     // FP8 block linears: fwd (K,K), dgrad (K,MN), wgrad (MN,MN); plus (K,K) for transposed-operand callers
     QTB_GEMM_CASE(0, false, false, EPI_BF16)
     QTB_GEMM_CASE(0, false, false, EPI_BF16_RES)
@@ -424,14 +543,55 @@ int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, i
     return 902;  // unsupported combination
 }
 
+// Tile configuration from a small cost model: for each (cta_group, BN) the
+// time is  waves x (per-SM tile work) / (per-SM rate), where the rate is the
+// tensor peak capped by this SM's share of L2 bandwidth times the tile's
+// arithmetic intensity (2*128*BN flops per (128 + BN/cg) operand rows).
+// QTB_GEMM_CG=1 forces single-CTA tiles.
+struct TileCfg {
+    int cg, bn;
+};
+TileCfg choose_cfg(int64_t M, int64_t N, int kind, bool b_mn) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("QTB_GEMM_CG");
+        forced = e ? atoi(e) : 0;
+    }
+    const int sms = num_sms();
+    const double elem = kind == 0 ? 1.0 : 2.0;
+    const double peak = kind == 0 ? 21.6e12 : 10.9e12;  // per SM, dense
+    const double l2 = 11.0e12 / sms;                   // bytes/s per SM (measured LTS cap, B300_MICROARCH.md)
+    TileCfg best{1, 256};
+    double best_t = 1e30;
+    for (int cg = 1; cg <= 2; ++cg) {
+        if (forced == 1 && cg == 2) continue;
+        if (cg == 2 && M < 256) continue;
+        for (int bn = 128; bn <= 256; bn += 128) {
+            if (cg == 2 && kind == 0 && b_mn && bn == 128) continue;  // half-atom MN-major B
+            const int64_t tiles = ceil_div(M, (int64_t)BM * cg) * ceil_div(N, bn);
+            const int64_t waves = ceil_div(tiles, sms / cg);
+            const double inten = 2.0 * BM * bn / ((BM + (double)bn / cg) * elem);
+            const double rate = std::min(peak, l2 * inten);
+            const double t = (double)waves * BM * bn / rate;
+            if (t < best_t * 0.999) {
+                best_t = t;
+                best = {cg, bn};
+            }
+        }
+    }
+    return best;
+}
+int pick_cg(int64_t M) { return choose_cfg(M, 1 << 20, 0, false).cg; }
+int pick_bn(int64_t N) { return choose_cfg(1 << 20, N, 0, false).bn; }
+
 // split-K factor for a GEMM (0 = no split): only when the tile grid leaves
 // most SMs idle and K is long enough to amortise the reduction
-int choose_splits(int64_t M, int64_t N, int64_t K, int kind, int bn) {
+int choose_splits(int64_t M, int64_t N, int64_t K, int kind, int bn, int cg) {
     const int bk = kind == 0 ? 128 : 64;
-    const int64_t tiles = ceil_div(M, BM) * ceil_div(N, bn);
+    const int64_t tiles = ceil_div(M, BM * cg) * ceil_div(N, bn);
     const int64_t nk = ceil_div(K, bk);
-    if (tiles * 2 > num_sms() || nk < 16) return 1;
-    int64_t s = num_sms() / tiles;
+    if (tiles * cg * 2 > num_sms() || nk < 16) return 1;
+    int64_t s = num_sms() / (tiles * cg);
     s = std::min<int64_t>(s, nk / 8);
     s = std::min<int64_t>(s, 8);
     return (int)std::max<int64_t>(s, 1);
@@ -443,9 +603,14 @@ int choose_splits(int64_t M, int64_t N, int64_t K, int kind, int bn) {
 using namespace qtb;
 
 extern "C" int qtk_gemm_splitk_ws_bytes(int64_t M, int64_t N, int64_t K, int kind) {
-    const int bn = N <= 128 ? 128 : 256;
-    const int s = qtb::gemm::choose_splits(M, N, K, kind, bn);
-    return s > 1 ? (int)std::min<int64_t>((int64_t)s * M * N * 4, INT32_MAX) : 0;
+    int best = 0;
+    for (int bmn = 0; bmn < 2; ++bmn) {  // the bound over both operand layouts
+        const auto tc = qtb::gemm::choose_cfg(M, N, kind, bmn != 0);
+        const int bn = (tc.cg == 2 && kind == 0 && bmn && tc.bn == 128) ? 256 : tc.bn;
+        const int s = qtb::gemm::choose_splits(M, N, K, kind, bn, tc.cg);
+        if (s > 1) best = std::max(best, (int)std::min<int64_t>((int64_t)s * M * N * 4, INT32_MAX));
+    }
+    return best;
 }
 
 extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
@@ -458,8 +623,11 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         ((g->lda * elem) & 15) || ((g->ldb * elem) & 15))
         return 1;
     if (g->lda < (g->a_mn ? g->M : g->K) || g->ldb < (g->b_mn ? g->N : g->K)) return 1;
-    int bn = g->bn;
-    if (bn != 128 && bn != 256) bn = g->N <= 128 ? 128 : 256;
+    const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0);
+    const int cg = tc.cg;
+    int bn = (g->bn == 128 || g->bn == 256) ? g->bn : tc.bn;
+    // FP8 MN-major B split over a CTA pair needs >= 128 N-columns per CTA
+    if (cg == 2 && g->kind == 0 && g->b_mn && bn == 128) bn = 256;
     Params p;
     memset(&p, 0, sizeof(p));
     int rc;
@@ -470,7 +638,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         rc = make_tmap(&p.ta, g->a, elem, g->M, g->K, g->lda, 128 / elem, bk);
     if (rc) return rc;
     if (!g->b_mn)
-        rc = make_tmap(&p.tb, g->b, elem, g->K, g->N, g->ldb, bk, bn);
+        rc = make_tmap(&p.tb, g->b, elem, g->K, g->N, g->ldb, bk, bn / cg);
     else
         rc = make_tmap(&p.tb, g->b, elem, g->N, g->K, g->ldb, 128 / elem, bk);
     if (rc) return rc;
@@ -486,12 +654,12 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     p.M = (int)g->M;
     p.N = (int)g->N;
     p.K = (int)g->K;
-    p.num_m = (int)ceil_div(g->M, BM);
+    p.num_m = (int)ceil_div(g->M, BM * cg);
     p.num_n = (int)ceil_div(g->N, bn);
     p.num_k = (int)ceil_div(g->K, bk);
     const uint32_t afmt = g->kind == 0 ? (uint32_t)g->a_fmt : 1u;  // bf16 = 1 in the F16 format table
     const uint32_t bfmt = g->kind == 0 ? (uint32_t)g->b_fmt : 1u;
-    p.idesc = sm100::make_idesc(afmt, bfmt, g->a_mn != 0, g->b_mn != 0, BM, bn);
+    p.idesc = sm100::make_idesc(afmt, bfmt, g->a_mn != 0, g->b_mn != 0, BM * cg, bn);
     p.a_scale = g->a_scale;
     p.b_scale = g->b_scale;
     p.out = g->out;
@@ -504,7 +672,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     const int tiles = p.num_m * p.num_n;
     int splits = 1;
     if (g->ws && g->split_k != 1) {
-        splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn);
+        splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn, cg);
         if ((int64_t)splits * g->M * g->N * 4 > g->ws_bytes) splits = 1;
     }
     p.splits = splits;
@@ -514,8 +682,8 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         p.out = g->ws;
         p.ldo = g->N;
         const int all = tiles * p.splits;
-        const int grid = all < num_sms() ? all : num_sms();
-        int rc2 = dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, EPI_F32, p, grid, s);
+        const int grid = std::min(all, num_sms() / cg) * cg;
+        int rc2 = dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, EPI_F32, p, grid, cg, s);
         if (rc2) return rc2;
         const int64_t total = g->M * g->N;
         const int rg = (int)std::min<int64_t>(ceil_div(total, 256), 8 * num_sms());
@@ -525,6 +693,6 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
                                                 g->sr_stream, g->sr_base);
         return (int)cudaGetLastError();
     }
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, s);
+    const int grid = std::min(tiles, num_sms() / cg) * cg;
+    return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, cg, s);
 }

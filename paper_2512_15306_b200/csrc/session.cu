@@ -194,6 +194,7 @@ class Session {
     float* dgamma = nullptr;
     float* rms_inv = nullptr;  // per-row 1/rms scratch of the forward norms
     float* Dv = nullptr;
+    float* attn_ws = nullptr;  // GQA per-head dK/dV partials
     float2* rope_tab = nullptr;
     int32_t *tok_buf = nullptr, *inputs = nullptr, *targets = nullptr, *sorted_pos = nullptr, *seg_tok = nullptr,
             *seg_off = nullptr;
@@ -434,6 +435,10 @@ class Session {
         req(&dgamma, d * 4);
         req(&rms_inv, M * 4);
         req(&Dv, (size_t)plan.micro_batch * H * T * 4);
+        {
+            const size_t wb = qtk_attn_bwd_ws_bytes(plan.micro_batch, T, H, Hkv, hd);
+            if (wb) req(&attn_ws, wb);
+        }
         req(&rope_tab, (size_t)T * (hd / 2) * 8);
         req(&tok_buf, (size_t)plan.ga_steps * plan.micro_batch * (T + 1) * 4);
         req(&inputs, M * 4);
@@ -794,7 +799,7 @@ class Session {
                  d_att, d);
             // ---- attention backward + inverse RoPE
             h = prof_begin();
-            QT_CHECK_K(qtk_attn_bwd(b.qkv, b.att32, d_att, d, b.lse, Dv, curB, curT, H, Hkv, hd, q, d_qkv, st));
+            QT_CHECK_K(qtk_attn_bwd(b.qkv, b.att32, d_att, d, b.lse, Dv, curB, curT, H, Hkv, hd, q, d_qkv, attn_ws, st));
             prof_end(h, 8, 10.0 * curB * H * (double)curT * curT / 2 * hd);
             h = prof_begin();
             QT_CHECK_K(qtk_rope(d_qkv, M, curT, H + Hkv, hd, q, rope_tab, 1, ga + G_DQKV, st));

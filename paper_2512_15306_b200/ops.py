@@ -175,7 +175,9 @@ def attn_bwd(qkv, out32, dout, lse, B, T, H, Hkv, hd):
     d = H * hd
     Dv = torch.empty((B, H, T), dtype=torch.float32, device=qkv.device)
     dqkv = torch.zeros_like(qkv)
+    wsb = _lib.lib().qtk_attn_bwd_ws_bytes(B, T, H, Hkv, hd)
+    ws = torch.empty(max(wsb // 4, 1), dtype=torch.float32, device=qkv.device)
     rc = _lib.lib().qtk_attn_bwd(_p(qkv), _p(out32), _p(dout), d, _p(lse), _p(Dv), B, T, H, Hkv, hd, qkv_dim,
-                                 _p(dqkv), _s())
+                                 _p(dqkv), _p(ws), _s())
     _lib.check(rc, "qtk_attn_bwd")
     return dqkv
