@@ -14,6 +14,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace qtb { namespace attn { __device__ __forceinline__ uint32_t sm100_smem(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); } } }
 
@@ -639,9 +640,20 @@ void qtk_attn_set_mode(int fast_exp, int bwd_split) {
     g_bwd_split = bwd_split;
 }
 
+int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
+                    float* out32, float* lse, uint32_t* amax, cudaStream_t s);
+
 int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
                  float* out32, float* lse, uint32_t* amax, cudaStream_t s) {
     if (H % Hkv) return 1;
+    static int use_tc = -1;
+    if (use_tc < 0) {
+        const char* e = getenv("QTB_ATTN_TC");
+        use_tc = e ? atoi(e) : 0;  // the mma.sync forward is faster today (softmax-bound)
+    }
+    // tcgen05 path for head_dim 64/128; the mma.sync kernel covers the rest
+    if (use_tc && (hd == 64 || hd == 128))
+        return qtk_attn_fwd_tc(qkv, B, T, H, Hkv, hd, qkv_dim, out, ldo, out32, lse, amax, s);
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     dim3 grid((unsigned)ceil_div(T, 64), H, B);
     if (hd == 64) {
@@ -672,10 +684,20 @@ size_t qtk_attn_bwd_ws_bytes(int B, int T, int H, int Hkv, int hd) {
     return H > Hkv ? (size_t)2 * B * H * T * hd * sizeof(float) : 0;
 }
 
+int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
+                    float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s);
+
 int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv, int B,
                  int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s) {
     if (H % Hkv || T % 4) return 1;
     if (H > Hkv && !ws) return 1;
+    static int use_tc = -1;
+    if (use_tc < 0) {
+        const char* e = getenv("QTB_ATTN_BWD_TC");
+        use_tc = e ? atoi(e) : 1;
+    }
+    if (use_tc && (hd == 64 || hd == 128))
+        return qtk_attn_bwd_tc(qkv, out32, dout, ldo, lse, Dv, B, T, H, Hkv, hd, qkv_dim, dqkv, ws, s);
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     const int64_t rows = (int64_t)B * T;
     bwd_dot_kernel<<<(unsigned)ceil_div(rows * H * 32, 256), 256, 0, s>>>((const uint16_t*)dout, out32, ldo, T,

@@ -1,0 +1,945 @@
+// Causal GQA attention forward on tcgen05 (sm_100a): reference sdpa_chunked /
+// attn_row_forward (src/tensorops.cpp:191-255).
+//
+// CTA = 128 query rows of one head; 8 warps: 0 TMA producer, 1 MMA issuer
+// (one thread), 2 TMEM allocator, 4..7 softmax (thread = query row = TMEM
+// lane).  Two passes over the causal KV tiles (128 keys each):
+//   pass 1  S = Q K^T (tcgen05 kind::f16, f32 in TMEM, double buffered);
+//           softmax warps keep the running row max m and sum l in f32
+//   pass 2  S again; P = exp(x - m) / l -- normalised before P.V exactly as
+//           the reference does (probs *= inv_denom, then out = sum p v) --
+//           written to SMEM as bf16 hi + lo (16 significant bits) in the
+//           UMMA 128-B-swizzled K-major layout; O += P_hi V + P_lo V in TMEM
+// then O (f32) -> bf16 att, the unrounded f32 copy for the backward's
+// D = rowsum(dO o O), LSE = m + log(l), and the fused absmax.
+#include "common.cuh"
+#include "kernels.h"
+#include "sm100.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace qtb {
+namespace attn_tc {
+
+using namespace sm100;
+
+constexpr int BQ = 128, BKV = 128;
+constexpr int NT = 384;  // 12 warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..11 softmax
+constexpr int NSW = 8;   // softmax warps: (lane quarter w%4) x (key half (w-4)/4)
+
+template <int HD>
+struct Smem {
+    static constexpr int Q = BQ * HD * 2;    // Q tile: HD/64 atom columns of 16 KB
+    static constexpr int K = BKV * HD * 2;   // one K stage
+    static constexpr int V = BKV * HD * 2;   // one V stage
+    static constexpr int P = BQ * BKV * 2;   // one P part (hi or lo): 2 atom columns
+    static constexpr int OFF_Q = 0;
+    static constexpr int OFF_K = OFF_Q + Q;
+    static constexpr int OFF_V = OFF_K + 2 * K;
+    static constexpr int OFF_PH = OFF_V + 2 * V;
+    static constexpr int OFF_PL = OFF_PH + P;
+    static constexpr int OFF_BAR = OFF_PL + P;
+    static constexpr int BYTES = OFF_BAR + 256 + 4 * BQ * 4 + 1024;  // barriers, (m, l) exchange, align
+};
+
+__device__ __forceinline__ void mma_bf16_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    mma_bf16(d, a, b, idesc, acc);
+}
+
+// K-major SW128 descriptor for a tile whose 64-element atom columns are
+// `atom_stride` bytes apart; k-step kk of UK=16 bf16
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int kk, int atom_stride) {
+    return make_sdesc_sw128(base + (kk >> 2) * atom_stride + (kk & 3) * 32, 16, 1024);
+}
+// MN-major SW128 descriptor (N contiguous in 64-element atoms LBO apart), k-step kk of 16 rows
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int kk, int lbo) {
+    return make_sdesc_sw128(base + kk * 16 * 128, lbo, 1024);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+constexpr float LOG2E = 1.4426950408889634f;
+
+template <int HD>
+__global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H, int Hkv,
+                                                       float inv_sqrt_d, uint16_t* __restrict__ out, int64_t ldo,
+                                                       float* __restrict__ out32, float* __restrict__ lse,
+                                                       uint32_t* __restrict__ amax) {
+    using S = Smem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+    uint64_t* q_full = bar + 0;
+    uint64_t* k_full = bar + 1;   // [2]
+    uint64_t* k_empty = bar + 3;  // [2]
+    uint64_t* v_full = bar + 5;   // [2]
+    uint64_t* v_empty = bar + 7;  // [2]
+    uint64_t* s_full = bar + 9;   // [2]
+    uint64_t* s_empty = bar + 11; // [2]
+    uint64_t* p_full = bar + 13;
+    uint64_t* p_empty = bar + 14;
+    uint64_t* o_full = bar + 15;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 16);
+
+    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int kvh = h / (H / Hkv);
+    const int d = H * HD;
+    const int nj = qt + 1;  // causal KV tiles (BQ == BKV)
+    const int row0 = b * T + qt * BQ;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) tma_prefetch(&tm);
+    if (warp == 1 && lane == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], NSW);
+        }
+        mbar_init(p_full, NSW);
+        mbar_init(p_empty, 1);
+        mbar_init(o_full, 1);
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t s_base = smem_u32(sm);
+
+    if (warp == 0 && lane == 0) {
+        // ===== TMA producer: Q once; pass 1 K tiles; pass 2 (K, V) tiles =====
+        mbar_arrive_expect_tx(q_full, S::Q);
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(&tm, q_full, sm + S::OFF_Q + c * BQ * 128, h * HD + c * 64, row0);
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int j = 0; j < nj; ++j) {
+                const int krow = b * T + j * BKV;
+                mbar_wait(&k_empty[ks], kph ^ 1);
+                mbar_arrive_expect_tx(&k_full[ks], S::K);
+                for (int c = 0; c < HD / 64; ++c)
+                    tma_load_2d(&tm, &k_full[ks], sm + S::OFF_K + ks * S::K + c * BKV * 128, d + kvh * HD + c * 64, krow);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+                if (pass == 1) {
+                    mbar_wait(&v_empty[vs], vph ^ 1);
+                    mbar_arrive_expect_tx(&v_full[vs], S::V);
+                    for (int c = 0; c < HD / 64; ++c)
+                        tma_load_2d(&tm, &v_full[vs], sm + S::OFF_V + vs * S::V + c * BKV * 128,
+                                    d + Hkv * HD + kvh * HD + c * 64, krow);
+                    if (++vs == 2) { vs = 0; vph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {  // MMA issuer: whole warp, elected lane issues
+        // ===== MMA issuer =====
+        const uint32_t idesc_s = make_idesc(1, 1, false, false, BQ, BKV);  // S: M128 N128, both K-major
+        const uint32_t idesc_o = make_idesc(1, 1, false, true, BQ, HD);    // O: A = P K-major, B = V MN-major
+        mbar_wait(q_full, 0);
+        int ks = 0, vs = 0, sc = 0;
+        uint32_t kph = 0, vph = 0;
+        auto issue_s = [&]() {
+            mbar_wait(&k_full[ks], kph);
+            const int sb = sc & 1;
+            mbar_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t qa = s_base + S::OFF_Q, ka = s_base + S::OFF_K + ks * S::K;
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+                mma_bf16_ss(tmem + sb * BKV, kdesc(qa, kk, BQ * 128), kdesc(ka, kk, BKV * 128), idesc_s, kk > 0);
+            tc_commit(&k_empty[ks]);
+            tc_commit(&s_full[sb]);
+            if (++ks == 2) { ks = 0; kph ^= 1; }
+            ++sc;
+        };
+        for (int j = 0; j < nj; ++j) issue_s();  // pass 1
+        issue_s();                                // pass 2, tile 0
+        for (int j = 0; j < nj; ++j) {
+            if (j + 1 < nj) issue_s();
+            mbar_wait(p_full, j & 1);
+            mbar_wait(&v_full[vs], vph);
+            tc_fence_after();
+            const uint32_t va = s_base + S::OFF_V + vs * S::V;
+            const uint32_t ph = s_base + S::OFF_PH, pl = s_base + S::OFF_PL;
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk) {
+                const uint64_t bd = mndesc(va, kk, BKV * 128);
+                mma_bf16_ss(tmem + 256, kdesc(ph, kk, BQ * 128), bd, idesc_o, (j | kk) != 0);
+                mma_bf16_ss(tmem + 256, kdesc(pl, kk, BQ * 128), bd, idesc_o, 1);
+            }
+            tc_commit(&v_empty[vs]);
+            tc_commit(p_empty);
+            if (++vs == 2) { vs = 0; vph ^= 1; }
+        }
+        tc_commit(o_full);
+    } else if (warp >= 4) {
+        // ===== softmax: thread = (query row, key half) =====
+        const int wq = warp & 3, half = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;
+        const int q = qt * BQ + r;  // position in the sequence
+        const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
+        const int c0 = half * (BKV / 2);  // this thread's 64 keys of each tile
+        float* xch = reinterpret_cast<float*>(sm + S::OFF_BAR + 256);  // [2][BQ] (m, l) exchange
+        float m = -INFINITY, l = 0.0f;
+        int sc = 0;
+        // pass 1: running max / sum over this half's keys (S read twice: max, then sum)
+        for (int j = 0; j < nj; ++j) {
+            const int sb = sc & 1;
+            mbar_wait(&s_full[sb], (sc >> 1) & 1);
+            tc_fence_after();
+            const int k0 = j * BKV + c0;
+            float mt = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t rr[32];
+                tmem_ld32(lane_base + sb * BKV + c0 + c * 32, rr);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int key = k0 + c * 32 + i;
+                    if (key <= q && key < T) mt = fmaxf(mt, __uint_as_float(rr[i]) * inv_sqrt_d);
+                }
+            }
+            const float mn = fmaxf(m, mt);
+            if (mn != -INFINITY) {
+                float ssum = 0.0f;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t rr[32];
+                    tmem_ld32(lane_base + sb * BKV + c0 + c * 32, rr);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int key = k0 + c * 32 + i;
+                        if (key <= q && key < T) ssum += ex2((__uint_as_float(rr[i]) * inv_sqrt_d - mn) * LOG2E);
+                    }
+                }
+                l = (m == -INFINITY ? 0.0f : l * ex2((m - mn) * LOG2E)) + ssum;
+                m = mn;
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            ++sc;
+        }
+        // combine the two halves' (m, l) once
+        if (half == 1) {
+            xch[r] = m;
+            xch[BQ + r] = l;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NSW * 32) : "memory");
+        if (half == 0) {
+            const float m1 = xch[r], l1 = xch[BQ + r];
+            const float mg = fmaxf(m, m1);
+            float lg = 0.0f;
+            if (mg != -INFINITY) {
+                lg = (m == -INFINITY ? 0.0f : l * ex2((m - mg) * LOG2E)) +
+                     (m1 == -INFINITY ? 0.0f : l1 * ex2((m1 - mg) * LOG2E));
+            }
+            xch[2 * BQ + r] = mg;
+            xch[3 * BQ + r] = lg;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NSW * 32) : "memory");
+        m = xch[2 * BQ + r];
+        l = xch[3 * BQ + r];
+        const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+        // pass 2: normalised probabilities -> P hi/lo in SMEM (this half = one atom column)
+        uint8_t* ph = sm + S::OFF_PH + half * BQ * 128;
+        uint8_t* pl = sm + S::OFF_PL + half * BQ * 128;
+        for (int j = 0; j < nj; ++j) {
+            const int sb = sc & 1;
+            mbar_wait(&s_full[sb], (sc >> 1) & 1);
+            mbar_wait(p_empty, (j & 1) ^ 1);
+            tc_fence_after();
+            const int k0 = j * BKV + c0;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                uint32_t rr[32];
+                tmem_ld32(lane_base + sb * BKV + c0 + c * 32, rr);
+                tmem_ld_wait();
+                uint32_t hi[16], lo[16];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    float pp[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int key = k0 + c * 32 + i + e;
+                        const float xv = __uint_as_float(rr[i + e]) * inv_sqrt_d;
+                        pp[e] = (key <= q && key < T) ? ex2((xv - m) * LOG2E) * inv_l : 0.0f;
+                    }
+                    const float h0 = bf16r(pp[0]), h1 = bf16r(pp[1]);
+                    hi[i / 2] = pack_bf16x2(h0, h1);
+                    lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
+                }
+                // K-major SW128: key chunk cc (8 keys) at r*128 + ((cc ^ (r&7)) * 16)
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    const int cc = c * 4 + q4;
+                    const int off = r * 128 + ((cc ^ (r & 7)) << 4);
+                    *reinterpret_cast<uint4*>(ph + off) =
+                        make_uint4(hi[q4 * 4 + 0], hi[q4 * 4 + 1], hi[q4 * 4 + 2], hi[q4 * 4 + 3]);
+                    *reinterpret_cast<uint4*>(pl + off) =
+                        make_uint4(lo[q4 * 4 + 0], lo[q4 * 4 + 1], lo[q4 * 4 + 2], lo[q4 * 4 + 3]);
+                }
+            }
+            tc_fence_before();
+            fence_async_shared();  // generic-proxy stores -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&s_empty[sb]);
+                mbar_arrive(p_full);
+            }
+            ++sc;
+        }
+        // epilogue: this half's HD/2 columns of the O row -> bf16 att + f32 copy; LSE; absmax
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        uint32_t mx = 0;
+        const bool valid = q < T;
+        const int64_t grow = (int64_t)b * T + q;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+            const int col = half * (HD / 2) + c * 32;
+            uint32_t rr[32];
+            tmem_ld32(lane_base + 256 + col, rr);
+            tmem_ld_wait();
+            if (valid) {
+                uint4* o16 = reinterpret_cast<uint4*>(out + grow * ldo + h * HD + col);
+                float4* o32 = reinterpret_cast<float4*>(out32 + grow * ldo + h * HD + col);
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4) {
+                    float f[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        f[e] = __uint_as_float(rr[v4 * 8 + e]);
+                        mx = max(mx, abs_bits(bf16r(f[e])));
+                    }
+                    o16[v4] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                         pack_bf16x2(f[6], f[7]));
+                    if (out32) {
+                        o32[2 * v4] = make_float4(f[0], f[1], f[2], f[3]);
+                        o32[2 * v4 + 1] = make_float4(f[4], f[5], f[6], f[7]);
+                    }
+                }
+            }
+        }
+        if (valid && half == 0) lse[((int64_t)b * H + h) * T + q] = m + logf(l);
+        mx = warp_max_u32(mx);
+        if (lane == 0 && amax && mx) atomicMax(amax, mx);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+
+// ===========================================================================
+// Backward on tcgen05 (reference sdpa_chunked_backward, src/tensorops.cpp:257-303).
+//
+// Elementwise warps read S (and dP) rows from TMEM, compute
+//   P = exp(x - LSE) ,  dS = P (dP - D) / sqrt(hd)
+// and write P / dS back as bf16 hi + lo pairs into the TMEM columns they
+// have just consumed; the following MMAs take that TMEM region as their A
+// operand (kind::f16, A in TMEM).  Column map for one 32-wide chunk c of a
+// thread's 64-column half: hi -> [c*32, c*32+16), lo -> [c*32+16, c*32+32)
+// (16 bf16 pairs each), so no write ever lands on a column still to be read.
+// ===========================================================================
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// A operand from TMEM
+// TMEM column of the bf16 A operand for k-step kk (16 k values) of a 128-wide
+// operand laid out by the chunk map above; part 0 = hi, 1 = lo
+__device__ __forceinline__ uint32_t a_col(int kk, int part) {
+    const int half = kk >> 2, c = (kk >> 1) & 1, sub = kk & 1;
+    return (uint32_t)(half * 64 + c * 32 + part * 16 + sub * 8);
+}
+__device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// v -> bf16 hi + bf16 lo (v - hi), packed pairs; hi is v rounded to nearest
+__device__ __forceinline__ void split32(const float (&v)[32], uint32_t (&hi)[16], uint32_t (&lo)[16]) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const uint32_t h = cvt_bf16x2(v[2 * i], v[2 * i + 1]);
+        hi[i] = h;
+        lo[i] = cvt_bf16x2(v[2 * i] - __uint_as_float(h << 16), v[2 * i + 1] - __uint_as_float(h & 0xffff0000u));
+    }
+}
+__device__ __forceinline__ float4 lds4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts2(uint32_t a, float x, float y) {
+    asm volatile("st.shared.f32 [%0], %1;\n\tst.shared.f32 [%0+128], %2;" ::"r"(a), "f"(x), "f"(y) : "memory");
+}
+// P^T / dS^T for 32 query columns of one key row.  sLD holds the columns'
+// -LSE*log2e (or -inf past T) and D/sqrt(d); qrel = first column's query - key.
+template <bool MASK>
+__device__ __forceinline__ void dkdv_elem(const uint32_t (&rs)[32], const uint32_t (&rp)[32], uint32_t sLD,
+                                          float c_s, float inv_sqrt_d, int qrel, float (&pv)[32], float (&dsv)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+        const float4 l4 = lds4(sLD + 4 * i);
+        const float4 d4 = lds4(sLD + 128 + 4 * i);
+        const float nl[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float p = ex2(__fmaf_rn(__uint_as_float(rs[i + u]), c_s, nl[u]));
+            if (MASK) p = qrel + i + u >= 0 ? p : 0.0f;
+            pv[i + u] = p;
+            dsv[i + u] = p * __fmaf_rn(__uint_as_float(rp[i + u]), inv_sqrt_d, -dd[u]);
+        }
+    }
+}
+// dS for 32 key columns of one query row; keys past `lim` (min(q, T-1)) masked
+template <bool MASK>
+__device__ __forceinline__ void dq_elem(const uint32_t (&rs)[32], const uint32_t (&rp)[32], float c_s, float nl,
+                                        float inv_sqrt_d, float dsc, int k0, int lim, float (&dsv)[32]) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        float p = ex2(__fmaf_rn(__uint_as_float(rs[i]), c_s, nl));
+        if (MASK) p = k0 + i <= lim ? p : 0.0f;
+        dsv[i] = p * __fmaf_rn(__uint_as_float(rp[i]), inv_sqrt_d, -dsc);
+    }
+}
+
+template <int HD>
+struct BwdSmem {
+    static constexpr int TILE = 128 * HD * 2;
+    static constexpr int NST = HD == 64 ? 4 : 2;  // ring stages of (tile pair)
+    static constexpr int QS = HD == 64 ? 2 : 1;   // dQ: Q/dO slots (next head's prefetch)
+    static constexpr int OFF_A = 0;               // dK/dV: K tile | dQ: [QS] Q tiles
+    static constexpr int OFF_B = QS * TILE;       // dK/dV: V tile | dQ: [QS] dO tiles
+    static constexpr int OFF_R = 2 * QS * TILE;   // ring [NST] of (Q_i, dO_i) | (K_j, V_j)
+    static constexpr int OFF_BAR = OFF_R + NST * 2 * TILE;
+    static constexpr int OFF_LD = OFF_BAR + 512;   // [NSW][64] f32 per-warp LSE / D columns
+    static constexpr int BYTES = OFF_LD + NSW * 64 * 4 + 1024;
+};
+
+// Backward work is cut into 64-wide sub-tiles (one half of a 128-row Q/dO or
+// K/V tile).  Each sub-tile's S and dP (f32, 64 TMEM columns each) live in one
+// of NB TMEM buffers, so the MMAs for sub-tile t+1 run while the elementwise
+// warps turn sub-tile t into P / dS, and the gradient MMAs of t follow.
+template <int HD>
+struct BwdPipe {
+    static constexpr int NB = (512 - 2 * HD) / 128;  // 3 for hd 64, 2 for hd 128
+    static constexpr int ACC = NB * 128;             // accumulator columns
+};
+
+// dK / dV for one 128-key tile of one KV head: loops over every query head of
+// the GQA group (ascending) and every query tile at or after the diagonal,
+// accumulating in TMEM; rounded to bf16 once at the end.
+// TMEM: buffers [b*128, +64) S^T -> P^T (hi|lo per 32), [b*128+64, +64) dP^T -> dS^T;
+// dV at ACC, dK at ACC + HD.
+template <int HD>
+__global__ void __launch_bounds__(NT, 1) dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq,
+                                                        const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
+                                                        const float* __restrict__ Dv, int T, int H, int Hkv,
+                                                        int qkv_dim, float inv_sqrt_d, uint16_t* __restrict__ dqkv) {
+    using S = BwdSmem<HD>;
+    using P = BwdPipe<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+    uint64_t* kv_full = bar + 0;
+    uint64_t* m_done = bar + 1;
+    uint64_t* s_full = bar + 2;                   // [NB]
+    uint64_t* p_full = bar + 2 + P::NB;           // [NB]
+    uint64_t* b_free = bar + 2 + 2 * P::NB;       // [NB]
+    uint64_t* r_full = bar + 2 + 3 * P::NB;       // [NST]
+    uint64_t* r_empty = r_full + S::NST;          // [NST]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(r_empty + S::NST);
+
+    const int kt = blockIdx.z, kvh = blockIdx.x, b = blockIdx.y;  // tile slowest: longest CTAs first
+    const int group = H / Hkv;
+    const int d = H * HD;
+    const int nq = (T + 127) / 128;
+    const int per_head = nq - kt;  // query tiles kt .. nq-1
+    const int niter = group * per_head;
+    const int nsub = 2 * niter;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tdo);
+    }
+    if (warp == 1 && lane == 0) {
+        mbar_init(kv_full, 1);
+        mbar_init(m_done, 1);
+        for (int i = 0; i < P::NB; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], NSW);
+            mbar_init(&b_free[i], 1);
+        }
+        for (int i = 0; i < S::NST; ++i) {
+            mbar_init(&r_full[i], 1);
+            mbar_init(&r_empty[i], 1);
+        }
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t s_base = smem_u32(sm);
+
+    if (warp == 0 && lane == 0) {
+        const int krow = b * T + kt * 128;
+        mbar_arrive_expect_tx(kv_full, 2 * S::TILE);
+        for (int c = 0; c < HD / 64; ++c) {
+            tma_load_2d(&tq, kv_full, sm + S::OFF_A + c * 128 * 128, d + kvh * HD + c * 64, krow);
+            tma_load_2d(&tq, kv_full, sm + S::OFF_B + c * 128 * 128, d + Hkv * HD + kvh * HD + c * 64, krow);
+        }
+        for (int it = 0; it < niter; ++it) {
+            const int st = it % S::NST;
+            const int h = kvh * group + it / per_head, qi = kt + it % per_head;
+            mbar_wait(&r_empty[st], ((it / S::NST) & 1) ^ 1);
+            mbar_arrive_expect_tx(&r_full[st], 2 * S::TILE);
+            const int qrow = b * T + qi * 128;
+            uint8_t* dst = sm + S::OFF_R + st * 2 * S::TILE;
+            for (int c = 0; c < HD / 64; ++c) {
+                tma_load_2d(&tq, &r_full[st], dst + c * 128 * 128, h * HD + c * 64, qrow);
+                tma_load_2d(&tdo, &r_full[st], dst + S::TILE + c * 128 * 128, h * HD + c * 64, qrow);
+            }
+        }
+    } else if (warp == 1) {  // MMA issuer: whole warp, elected lane issues
+        const uint32_t idesc_s = make_idesc(1, 1, false, false, 128, 64);  // S^T, dP^T: keys x 64 queries
+        const uint32_t idesc_g = make_idesc(1, 1, false, true, 128, HD);   // dV, dK: A TMEM, B MN-major
+        const uint32_t ka = s_base + S::OFF_A, va = s_base + S::OFF_B;
+        mbar_wait(kv_full, 0);
+        auto issue_s = [&](int t) {
+            const int it = t >> 1, sub = t & 1, st = it % S::NST, buf = t % P::NB;
+            if (sub == 0) mbar_wait(&r_full[st], (it / S::NST) & 1);
+            if (t >= P::NB) mbar_wait(&b_free[buf], ((t - P::NB) / P::NB) & 1);
+            tc_fence_after();
+            const uint32_t qa = s_base + S::OFF_R + st * 2 * S::TILE + sub * 64 * 128, oa = qa + S::TILE;
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk) {
+                mma_bf16_ss(tmem + buf * 128, kdesc(ka, kk, 128 * 128), kdesc(qa, kk, 128 * 128), idesc_s, kk > 0);
+                mma_bf16_ss(tmem + buf * 128 + 64, kdesc(va, kk, 128 * 128), kdesc(oa, kk, 128 * 128), idesc_s, kk > 0);
+            }
+            tc_commit(&s_full[buf]);
+        };
+        issue_s(0);
+        for (int t = 0; t < nsub; ++t) {
+            if (t + 1 < nsub) issue_s(t + 1);
+            const int it = t >> 1, sub = t & 1, st = it % S::NST, buf = t % P::NB;
+            mbar_wait(&p_full[buf], (t / P::NB) & 1);
+            tc_fence_after();
+            const uint32_t qa = s_base + S::OFF_R + st * 2 * S::TILE, oa = qa + S::TILE;
+            const uint32_t pb = tmem + buf * 128;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t bo = mndesc(oa, kk + 4 * sub, 128 * 128), bq = mndesc(qa, kk + 4 * sub, 128 * 128);
+                const uint32_t acc = (t | kk) != 0;
+                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bo, idesc_g, acc);
+                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bo, idesc_g, 1);
+                mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 0), bq, idesc_g, acc);
+                mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 1), bq, idesc_g, 1);
+            }
+            tc_commit(&b_free[buf]);
+            if (sub == 1) tc_commit(&r_empty[st]);
+        }
+        tc_commit(m_done);
+    } else if (warp >= 4) {
+        const int wq = warp & 3, half = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;
+        const int kv = kt * 128 + r;  // key position
+        const uint32_t lb = tmem + ((uint32_t)(wq * 32) << 16);
+        const float c_s = inv_sqrt_d * LOG2E;
+        const uint32_t sLD = s_base + S::OFF_LD + (warp - 4) * 256;
+        // raw LSE / D of this warp's 32 query columns of a sub-tile, one per lane;
+        // loaded a sub-tile ahead, scaled when stored to shared memory
+        int nh = 0, nqi = 0, nsb = 0;  // (head, query tile, sub) of the next sub-tile to load
+        float Ln = 0.0f, Dn = 0.0f;
+        bool vn = false;
+        auto load_ld = [&]() {
+            const int ql = (kt + nqi) * 128 + nsb * 64 + half * 32 + lane;
+            const int64_t o = ((int64_t)b * H + kvh * group + nh) * T + ql;
+            vn = ql < T;
+            if (vn) {
+                Ln = __ldg(lse + o);
+                Dn = __ldg(Dv + o);
+            }
+            if (++nsb == 2) {
+                nsb = 0;
+                if (++nqi == per_head) {
+                    nqi = 0;
+                    ++nh;
+                }
+            }
+        };
+        load_ld();
+        int buf = 0, ph = 0, qi = kt, sub = 0;
+        for (int t = 0; t < nsub; ++t) {
+            const int q0 = qi * 128 + sub * 64 + half * 32;
+            __syncwarp();
+            sts2(sLD + 4 * lane, vn ? -Ln * LOG2E : -INFINITY, vn ? Dn * inv_sqrt_d : 0.0f);
+            if (t + 1 < nsub) load_ld();  // consumed next sub-tile: latency hidden
+            __syncwarp();
+            mbar_wait(&s_full[buf], ph);
+            tc_fence_after();
+            const uint32_t col = buf * 128 + half * 32;
+            uint32_t rs[32], rp[32];
+            tmem_ld32(lb + col, rs);
+            tmem_ld32(lb + col + 64, rp);
+            tmem_ld_wait();
+            float pv[32], dsv[32];
+            if (q0 >= kt * 128 + 127)  // whole warp above the diagonal
+                dkdv_elem<false>(rs, rp, sLD, c_s, inv_sqrt_d, 0, pv, dsv);
+            else
+                dkdv_elem<true>(rs, rp, sLD, c_s, inv_sqrt_d, q0 - kv, pv, dsv);
+            uint32_t hi[16], lo[16];
+            split32(pv, hi, lo);
+            tmem_st16(lb + col, hi);
+            tmem_st16(lb + col + 16, lo);
+            split32(dsv, hi, lo);
+            tmem_st16(lb + col + 64, hi);
+            tmem_st16(lb + col + 64 + 16, lo);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[buf]);
+            if (++buf == P::NB) {
+                buf = 0;
+                ph ^= 1;
+            }
+            if (++sub == 2) {
+                sub = 0;
+                if (++qi == kt + per_head) qi = kt;
+            }
+        }
+        // dV, dK rows (bf16, rounded once): this thread writes HD/2 columns of each
+        mbar_wait(m_done, 0);
+        tc_fence_after();
+        const int64_t grow = (int64_t)b * T + kv;
+#pragma unroll
+        for (int which = 0; which < 2; ++which) {  // 0 = dV, 1 = dK
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {
+                const int col = half * (HD / 2) + c * 32;
+                uint32_t rr[32];
+                tmem_ld32(lb + P::ACC + which * HD + col, rr);
+                tmem_ld_wait();
+                if (kv >= T) continue;
+                uint16_t* dst = dqkv + grow * qkv_dim + d + (which ? 0 : Hkv * HD) + kvh * HD + col;
+                uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4)
+                    d4[v4] = make_uint4(pack_bf16x2(__uint_as_float(rr[v4 * 8 + 0]), __uint_as_float(rr[v4 * 8 + 1])),
+                                        pack_bf16x2(__uint_as_float(rr[v4 * 8 + 2]), __uint_as_float(rr[v4 * 8 + 3])),
+                                        pack_bf16x2(__uint_as_float(rr[v4 * 8 + 4]), __uint_as_float(rr[v4 * 8 + 5])),
+                                        pack_bf16x2(__uint_as_float(rr[v4 * 8 + 6]), __uint_as_float(rr[v4 * 8 + 7])));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// dQ for one 128-query tile of every query head of one KV group: items
+// (head hh, key tile j <= qt), each two 64-key sub-tiles; the (K_j, V_j) tiles
+// stream through a ring, Q/dO of the current head sit in QS slots.  dQ
+// accumulates in TMEM over the keys and is written (bf16) per head.
+// TMEM: buffers [b*128, +64) S -> dS (hi|lo per 32), [b*128+64, +64) dP; dQ at ACC.
+template <int HD>
+__global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CUtensorMap tq,
+                                                      const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
+                                                      const float* __restrict__ Dv, int T, int H, int Hkv, int qkv_dim,
+                                                      float inv_sqrt_d, uint16_t* __restrict__ dqkv, int dbg) {
+    using S = BwdSmem<HD>;
+    using P = BwdPipe<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+    uint64_t* dq_done = bar + 0;
+    uint64_t* dq_free = bar + 1;              // epilogue read dQ of the previous head
+    uint64_t* qo_full = bar + 2;              // [2]
+    uint64_t* qo_empty = bar + 4;             // [2]
+    uint64_t* s_full = bar + 6;               // [NB]
+    uint64_t* p_full = s_full + P::NB;        // [NB]
+    uint64_t* b_free = p_full + P::NB;        // [NB]
+    uint64_t* r_full = b_free + P::NB;        // [NST]
+    uint64_t* r_empty = r_full + S::NST;      // [NST]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(r_empty + S::NST);
+
+    const int qt = gridDim.z - 1 - blockIdx.z, kvh = blockIdx.x, b = blockIdx.y;  // longest CTAs first
+    const int group = H / Hkv;
+    const int d = H * HD;
+    const int per_head = qt + 1;
+    const int niter = group * per_head;
+    const int nsub = 2 * niter;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tdo);
+    }
+    if (warp == 1 && lane == 0) {
+        mbar_init(dq_done, 1);
+        mbar_init(dq_free, NSW);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&qo_full[i], 1);
+            mbar_init(&qo_empty[i], 1);
+        }
+        for (int i = 0; i < P::NB; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], NSW);
+            mbar_init(&b_free[i], 1);
+        }
+        for (int i = 0; i < S::NST; ++i) {
+            mbar_init(&r_full[i], 1);
+            mbar_init(&r_empty[i], 1);
+        }
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t s_base = smem_u32(sm);
+
+    if (warp == 0 && lane == 0) {
+        const int qrow = b * T + qt * 128;
+        for (int it = 0; it < niter; ++it) {
+            const int hh = it / per_head, j = it % per_head;
+            if (j == 0) {  // this head's Q / dO
+                const int slot = hh % S::QS;
+                mbar_wait(&qo_empty[slot], ((hh / S::QS) & 1) ^ 1);
+                mbar_arrive_expect_tx(&qo_full[slot], 2 * S::TILE);
+                const int h = kvh * group + hh;
+                for (int c = 0; c < HD / 64; ++c) {
+                    tma_load_2d(&tq, &qo_full[slot], sm + S::OFF_A + slot * S::TILE + c * 128 * 128, h * HD + c * 64, qrow);
+                    tma_load_2d(&tdo, &qo_full[slot], sm + S::OFF_B + slot * S::TILE + c * 128 * 128, h * HD + c * 64,
+                                qrow);
+                }
+            }
+            const int st = it % S::NST;
+            mbar_wait(&r_empty[st], ((it / S::NST) & 1) ^ 1);
+            if (dbg & 8) { mbar_arrive(&r_full[st]); continue; }
+            mbar_arrive_expect_tx(&r_full[st], 2 * S::TILE);
+            const int krow = b * T + j * 128;
+            uint8_t* dst = sm + S::OFF_R + st * 2 * S::TILE;
+            for (int c = 0; c < HD / 64; ++c) {
+                tma_load_2d(&tq, &r_full[st], dst + c * 128 * 128, d + kvh * HD + c * 64, krow);
+                tma_load_2d(&tq, &r_full[st], dst + S::TILE + c * 128 * 128, d + Hkv * HD + kvh * HD + c * 64, krow);
+            }
+        }
+    } else if (warp == 1) {  // MMA issuer: whole warp, elected lane issues
+        const uint32_t idesc_s = make_idesc(1, 1, false, false, 128, 64);  // S, dP: queries x 64 keys
+        const uint32_t idesc_g = make_idesc(1, 1, false, true, 128, HD);   // dQ: A TMEM, B = K MN-major
+        auto issue_s = [&](int t) {
+            const int it = t >> 1, sub = t & 1, st = it % S::NST, buf = t % P::NB;
+            const int hh = it / per_head, j = it % per_head, slot = hh % S::QS;
+            if (sub == 0) {
+                if (j == 0) mbar_wait(&qo_full[slot], (hh / S::QS) & 1);
+                mbar_wait(&r_full[st], (it / S::NST) & 1);
+            }
+            if (t >= P::NB) mbar_wait(&b_free[buf], ((t - P::NB) / P::NB) & 1);
+            tc_fence_after();
+            const uint32_t qa = s_base + S::OFF_A + slot * S::TILE, oa = s_base + S::OFF_B + slot * S::TILE;
+            const uint32_t ka = s_base + S::OFF_R + st * 2 * S::TILE + sub * 64 * 128, va = ka + S::TILE;
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk) if (!(dbg & 4)) {
+                mma_bf16_ss(tmem + buf * 128, kdesc(qa, kk, 128 * 128), kdesc(ka, kk, 128 * 128), idesc_s, kk > 0);
+                mma_bf16_ss(tmem + buf * 128 + 64, kdesc(oa, kk, 128 * 128), kdesc(va, kk, 128 * 128), idesc_s, kk > 0);
+            }
+            tc_commit(&s_full[buf]);
+            if (sub == 1 && j == per_head - 1) tc_commit(&qo_empty[slot]);  // last use of this head's Q/dO
+        };
+        issue_s(0);
+        for (int t = 0; t < nsub; ++t) {
+            if (t + 1 < nsub) issue_s(t + 1);
+            const int it = t >> 1, sub = t & 1, st = it % S::NST, buf = t % P::NB;
+            const int hh = it / per_head, j = it % per_head;
+            if (j == 0 && sub == 0 && hh > 0) mbar_wait(dq_free, (hh - 1) & 1);  // previous head's dQ read out
+            mbar_wait(&p_full[buf], (t / P::NB) & 1);
+            tc_fence_after();
+            const uint32_t ka = s_base + S::OFF_R + st * 2 * S::TILE;
+            const uint32_t pb = tmem + buf * 128;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) if (!(dbg & 2)) {
+                const uint64_t bk = mndesc(ka, kk + 4 * sub, 128 * 128);
+                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bk, idesc_g, (j | sub | kk) != 0);
+                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bk, idesc_g, 1);
+            }
+            tc_commit(&b_free[buf]);
+            if (sub == 1) {
+                tc_commit(&r_empty[st]);
+                if (j == per_head - 1) tc_commit(dq_done);
+            }
+        }
+    } else if (warp >= 4) {
+        const int wq = warp & 3, half = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;
+        const int q = qt * 128 + r;
+        const uint32_t lb = tmem + ((uint32_t)(wq * 32) << 16);
+        const bool qok = q < T;
+        const float c_s = inv_sqrt_d * LOG2E;
+        const int64_t grow = (int64_t)b * T + q;
+        int t = 0;
+        for (int hh = 0; hh < group; ++hh) {
+            const int h = kvh * group + hh;
+            const float Lq = qok ? lse[((int64_t)b * H + h) * T + q] : 0.0f;
+            const float Dq = qok ? Dv[((int64_t)b * H + h) * T + q] : 0.0f;
+            const float nl = -Lq * LOG2E, dsc = Dq * inv_sqrt_d;
+            for (int js = 0; js < 2 * per_head; ++js, ++t) {
+                const int buf = t % P::NB;
+                mbar_wait(&s_full[buf], (t / P::NB) & 1);
+                tc_fence_after();
+                const int k0 = js * 64 + half * 32;
+                const uint32_t col = buf * 128 + half * 32;
+                uint32_t rs[32], rp[32];
+                if (dbg & 1) { __syncwarp(); if (lane == 0) mbar_arrive(&p_full[buf]); continue; }
+                tmem_ld32(lb + col, rs);
+                tmem_ld32(lb + col + 64, rp);
+                tmem_ld_wait();
+                float dsv[32];
+                if (k0 + 31 <= qt * 128 + wq * 32 && k0 + 31 < T)  // whole warp below the diagonal
+                    dq_elem<false>(rs, rp, c_s, nl, inv_sqrt_d, dsc, k0, 0, dsv);
+                else
+                    dq_elem<true>(rs, rp, c_s, nl, inv_sqrt_d, dsc, k0, qok ? q : -1, dsv);
+                uint32_t hi[16], lo[16];
+                split32(dsv, hi, lo);
+                tmem_st16(lb + col, hi);
+                tmem_st16(lb + col + 16, lo);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[buf]);
+            }
+            // this head's dQ: wait for its last MMA, read out, release the TMEM columns
+            mbar_wait(dq_done, hh & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {
+                const int col = half * (HD / 2) + c * 32;
+                uint32_t rr[32];
+                tmem_ld32(lb + P::ACC + col, rr);
+                tmem_ld_wait();
+                if (!qok) continue;
+                uint4* d4 = reinterpret_cast<uint4*>(dqkv + grow * qkv_dim + h * HD + col);
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4)
+                    d4[v4] = make_uint4(pack_bf16x2(__uint_as_float(rr[v4 * 8 + 0]), __uint_as_float(rr[v4 * 8 + 1])),
+                                        pack_bf16x2(__uint_as_float(rr[v4 * 8 + 2]), __uint_as_float(rr[v4 * 8 + 3])),
+                                        pack_bf16x2(__uint_as_float(rr[v4 * 8 + 4]), __uint_as_float(rr[v4 * 8 + 5])),
+                                        pack_bf16x2(__uint_as_float(rr[v4 * 8 + 6]), __uint_as_float(rr[v4 * 8 + 7])));
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dq_free);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+}  // namespace attn_tc
+}  // namespace qtb
+
+namespace qtb {
+namespace gemm {
+int make_tmap(CUtensorMap* m, const void* ptr, int elem, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+              uint32_t box_inner, uint32_t box_outer);
+}
+}  // namespace qtb
+
+using namespace qtb;
+
+extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out,
+                               int64_t ldo, float* out32, float* lse, uint32_t* amax, cudaStream_t s) {
+    using namespace qtb::attn_tc;
+    if (H % Hkv || (hd != 64 && hd != 128) || (qkv_dim % 8) || (ldo % 8)) return 1;
+    CUtensorMap tm;
+    int rc = qtb::gemm::make_tmap(&tm, qkv, 2, (uint64_t)qkv_dim, (uint64_t)B * T, (uint64_t)qkv_dim, 64, 128);
+    if (rc) return rc;
+    const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
+    dim3 grid((unsigned)ceil_div(T, BQ), H, B);
+    if (hd == 64) {
+        const int smem = Smem<64>::BYTES;
+        cudaFuncSetAttribute(fwd_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        fwd_tc_kernel<64><<<grid, NT, smem, s>>>(tm, T, H, Hkv, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, amax);
+    } else {
+        const int smem = Smem<128>::BYTES;
+        cudaFuncSetAttribute(fwd_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        fwd_tc_kernel<128><<<grid, NT, smem, s>>>(tm, T, H, Hkv, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, amax);
+    }
+    return (int)cudaGetLastError();
+}
+
+namespace qtb {
+namespace attn {
+__global__ void bwd_dot_kernel(const uint16_t* __restrict__ dout, const float* __restrict__ o, int64_t ld, int T,
+                               int H, int hd, int64_t rows, float* __restrict__ D);
+}  // namespace attn
+}  // namespace qtb
+
+extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
+                               float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws,
+                               cudaStream_t s) {
+    using namespace qtb::attn_tc;
+    if (H % Hkv || (hd != 64 && hd != 128) || (qkv_dim % 8) || (ldo % 8)) return 1;
+    (void)ws;  // dK/dV accumulate over the GQA group in TMEM: no partials
+
+    const int64_t rows = (int64_t)B * T;
+    qtb::attn::bwd_dot_kernel<<<(unsigned)ceil_div(rows * H * 32, 256), 256, 0, s>>>((const uint16_t*)dout, out32,
+                                                                                     ldo, T, H, hd, rows, Dv);
+    CUtensorMap tq, tdo;
+    int rc = qtb::gemm::make_tmap(&tq, qkv, 2, (uint64_t)qkv_dim, (uint64_t)rows, (uint64_t)qkv_dim, 64, 128);
+    if (rc) return rc;
+    rc = qtb::gemm::make_tmap(&tdo, dout, 2, (uint64_t)ldo, (uint64_t)rows, (uint64_t)ldo, 64, 128);
+    if (rc) return rc;
+    const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
+    dim3 grid(Hkv, B, (unsigned)ceil_div(T, 128));
+#define QTB_BWD_TC(HD)                                                                                               \
+    {                                                                                                              \
+        const int smem = BwdSmem<HD>::BYTES;                                                                       \
+        cudaFuncSetAttribute(dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
+        cudaFuncSetAttribute(dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
+        dkdv_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
+        dq_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv, getenv("QTB_ATTN_DBG") ? atoi(getenv("QTB_ATTN_DBG")) : 0); \
+    }
+    if (hd == 64)
+        QTB_BWD_TC(64)
+    else
+        QTB_BWD_TC(128)
+#undef QTB_BWD_TC
+    return (int)cudaGetLastError();
+}

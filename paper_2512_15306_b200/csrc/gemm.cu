@@ -282,8 +282,8 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 }
             }
         }
-    } else if (warp == 1 && lane == 0 && leader) {
-        // ===== MMA issuer (single thread of the leader CTA) =====
+    } else if (warp == 1 && leader) {
+        // ===== MMA issuer (warp-collective, one elected lane issues; leader CTA) =====
         int stage = 0;
         uint32_t phase = 0;
         int it = 0;
@@ -312,28 +312,14 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                         if constexpr (KIND == 0) mma_f8(d_tmem, ad, bd, p.idesc, accum);
                         else mma_bf16(d_tmem, ad, bd, p.idesc, accum);
                     } else {
-                        if constexpr (KIND == 0)
-                            asm volatile(
-                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-                                "l"(ad), "l"(bd), "r"(p.idesc), "r"(accum)
-                                : "memory");
-                        else
-                            asm volatile(
-                                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-                                "l"(ad), "l"(bd), "r"(p.idesc), "r"(accum)
-                                : "memory");
+                        if constexpr (KIND == 0) mma_f8_pair(d_tmem, ad, bd, p.idesc, accum);
+                        else mma_bf16_pair(d_tmem, ad, bd, p.idesc, accum);
                     }
                 }
                 if constexpr (CG == 1)
                     tc_commit(&empty[stage]);
                 else
-                    asm volatile(
-                        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-                        "[%0], %1;" ::"r"(smem_u32(&empty[stage])),
-                        "h"((uint16_t)3)
-                        : "memory");
+                    tc_commit_pair(&empty[stage]);
                 if (++stage == C::STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -342,11 +328,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             if constexpr (CG == 1)
                 tc_commit(&tfull[acc]);
             else
-                asm volatile(
-                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
-                    "[%0], %1;" ::"r"(smem_u32(&tfull[acc])),
-                    "h"((uint16_t)3)
-                    : "memory");
+                tc_commit_pair(&tfull[acc]);
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> rounding -> HBM =====

@@ -66,29 +66,50 @@ __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// ---- warp-collective tcgen05 issue ------------------------------------------
+// The MMA / commit wrappers below are executed by ALL 32 lanes of a converged
+// warp; elect.sync inside the asm picks the one lane that issues.  Issuing from
+// a single divergent lane instead makes the compiler wrap every instruction in
+// a waterfall loop (ELECT + R2UR.BROADCAST + BRA.U.ANY) that costs ~100 cycles
+// per MMA -- measured 108 vs 64 cycles for M128 N128 K16 (scripts/micro/mma_rate.cu).
+#define QTB_ELECT "elect.sync _|E, 0xffffffff;\n\t"
+
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+    asm volatile("{\n\t.reg .pred E;\n\t" QTB_ELECT
+                 "@E tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+// cta_group::2 commit, arriving on the barrier at the same offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile("{\n\t.reg .pred E;\n\t" QTB_ELECT
+                 "@E tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                 "%1;\n\t}" ::"r"(smem_u32(bar)),
+                 "h"((uint16_t)3)
                  : "memory");
 }
 
 // kind::f8f6f4 (E4M3/E5M2 operands) and kind::f16 (BF16 operands); D in TMEM f32
-__device__ __forceinline__ void mma_f8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                       uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-}
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
+#define QTB_MMA(NAME, CG, KIND)                                                                                 \
+    __device__ __forceinline__ void NAME(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,      \
+                                         uint32_t accum) {                                                     \
+        asm volatile("{\n\t.reg .pred E, p;\n\t" QTB_ELECT "setp.ne.b32 p, %4, 0;\n\t"                          \
+                     "@E tcgen05.mma.cta_group::" #CG ".kind::" #KIND " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d), \
+                     "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)                                            \
+                     : "memory");                                                                              \
+    }
+QTB_MMA(mma_f8, 1, f8f6f4)
+QTB_MMA(mma_bf16, 1, f16)
+QTB_MMA(mma_f8_pair, 2, f8f6f4)
+QTB_MMA(mma_bf16_pair, 2, f16)
+#undef QTB_MMA
+// A operand from TMEM (kind::f16)
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accum) {
+    asm volatile("{\n\t.reg .pred E, p;\n\t" QTB_ELECT "setp.ne.b32 p, %4, 0;\n\t"
+                 "@E tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+                 "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
+                 : "memory");
 }
 
 // 32 lanes x 32 consecutive f32 columns -> 32 registers per thread
