@@ -676,7 +676,7 @@ template <int HD>
 __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                       const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                                                       const float* __restrict__ Dv, int T, int H, int Hkv, int qkv_dim,
-                                                      float inv_sqrt_d, uint16_t* __restrict__ dqkv, int dbg) {
+                                                      float inv_sqrt_d, uint16_t* __restrict__ dqkv) {
     using S = BwdSmem<HD>;
     using P = BwdPipe<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -748,7 +748,6 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
             }
             const int st = it % S::NST;
             mbar_wait(&r_empty[st], ((it / S::NST) & 1) ^ 1);
-            if (dbg & 8) { mbar_arrive(&r_full[st]); continue; }
             mbar_arrive_expect_tx(&r_full[st], 2 * S::TILE);
             const int krow = b * T + j * 128;
             uint8_t* dst = sm + S::OFF_R + st * 2 * S::TILE;
@@ -772,7 +771,7 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
             const uint32_t qa = s_base + S::OFF_A + slot * S::TILE, oa = s_base + S::OFF_B + slot * S::TILE;
             const uint32_t ka = s_base + S::OFF_R + st * 2 * S::TILE + sub * 64 * 128, va = ka + S::TILE;
 #pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) if (!(dbg & 4)) {
+            for (int kk = 0; kk < HD / 16; ++kk) {
                 mma_bf16_ss(tmem + buf * 128, kdesc(qa, kk, 128 * 128), kdesc(ka, kk, 128 * 128), idesc_s, kk > 0);
                 mma_bf16_ss(tmem + buf * 128 + 64, kdesc(oa, kk, 128 * 128), kdesc(va, kk, 128 * 128), idesc_s, kk > 0);
             }
@@ -790,7 +789,7 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
             const uint32_t ka = s_base + S::OFF_R + st * 2 * S::TILE;
             const uint32_t pb = tmem + buf * 128;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) if (!(dbg & 2)) {
+            for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t bk = mndesc(ka, kk + 4 * sub, 128 * 128);
                 mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bk, idesc_g, (j | sub | kk) != 0);
                 mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bk, idesc_g, 1);
@@ -822,7 +821,6 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
                 const int k0 = js * 64 + half * 32;
                 const uint32_t col = buf * 128 + half * 32;
                 uint32_t rs[32], rp[32];
-                if (dbg & 1) { __syncwarp(); if (lane == 0) mbar_arrive(&p_full[buf]); continue; }
                 tmem_ld32(lb + col, rs);
                 tmem_ld32(lb + col + 64, rp);
                 tmem_ld_wait();
@@ -934,7 +932,7 @@ extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* 
         cudaFuncSetAttribute(dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
         cudaFuncSetAttribute(dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
         dkdv_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
-        dq_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv, getenv("QTB_ATTN_DBG") ? atoi(getenv("QTB_ATTN_DBG")) : 0); \
+        dq_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
     }
     if (hd == 64)
         QTB_BWD_TC(64)

@@ -52,19 +52,29 @@ __global__ void __launch_bounds__(CE_T) ce_softmax_kernel(const float* __restric
     const float* l = logits + row * ldl;
     const int V4 = V / 4;
     const float4* l4 = reinterpret_cast<const float4*>(l);
-    float mx = -INFINITY;
+    // one pass for (max, sum exp): each thread keeps a running max and rescales
+    // its partial sum when the max grows; partials meet at the block max
+    float mx = -INFINITY, s = 0.0f;
     for (int i = threadIdx.x; i < V4; i += CE_T) {
         const float4 v = l4[i];
-        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-    }
-    for (int i = V4 * 4 + threadIdx.x; i < V; i += CE_T) mx = fmaxf(mx, l[i]);
-    mx = block_reduce_max(mx, red);
-    float s = 0.0f;
-    for (int i = threadIdx.x; i < V4; i += CE_T) {
-        const float4 v = l4[i];
+        const float m4 = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+        if (m4 > mx) {
+            s *= expf(mx - m4);
+            mx = m4;
+        }
         s += expf(v.x - mx) + expf(v.y - mx) + expf(v.z - mx) + expf(v.w - mx);
     }
-    for (int i = V4 * 4 + threadIdx.x; i < V; i += CE_T) s += expf(l[i] - mx);
+    for (int i = V4 * 4 + threadIdx.x; i < V; i += CE_T) {
+        const float x = l[i];
+        if (x > mx) {
+            s *= expf(mx - x);
+            mx = x;
+        }
+        s += expf(x - mx);
+    }
+    const float bmx = block_reduce_max(mx, red);
+    if (mx != -INFINITY) s *= expf(mx - bmx);
+    mx = bmx;
     const float denom = block_reduce_sum(s, red);
     const int tgt = targets[row];
     if (threadIdx.x == 0) loss_rows[row] = (mx + logf(denom)) - l[tgt];
@@ -256,6 +266,8 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
     const float one_m_b1 = __fsub_rn(1.0f, h.b1), one_m_b2 = __fsub_rn(1.0f, h.b2);
     const float gscale = *h.grad_scale;
     const int64_t end = min(sg.n, ch.start + (int64_t)ADAM_CHUNK);
+    const uint64_t kw = rng_key(h.seed, sg.sw);
+    const uint64_t km = h.bf16_moments ? rng_key(h.seed, sg.sm) : 0, kv = h.bf16_moments ? rng_key(h.seed, sg.sv) : 0;
     uint32_t amax = 0;
     bool bad = false;
     for (int64_t j0 = ch.start + threadIdx.x * 8; j0 < end; j0 += ADAM_T * 8) {
@@ -285,13 +297,13 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
             const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), h.eps)), __fmul_rn(h.wd, pv[k]));
             const float p_new = __fsub_rn(pv[k], __fmul_rn(h.lr, upd));
             if (h.bf16_moments) {
-                mv[k] = sr_bf16(m_new, h.seed, sg.sm, ctr0 + k);
-                vv[k] = sr_bf16(v_new, h.seed, sg.sv, ctr0 + k);
+                mv[k] = sr_bf16k(m_new, km, ctr0 + k);
+                vv[k] = sr_bf16k(v_new, kv, ctr0 + k);
             } else {
                 mv[k] = m_new;
                 vv[k] = v_new;
             }
-            pv[k] = sr_bf16(p_new, h.seed, sg.sw, ctr0 + k);
+            pv[k] = sr_bf16k(p_new, kw, ctr0 + k);
             amax = max(amax, abs_bits(pv[k]));
         }
         if (cnt == 8 && (pi & 7) == 0 && (i & 7) == 0) {

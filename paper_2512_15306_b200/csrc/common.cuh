@@ -97,23 +97,46 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
     z ^= z >> 31;
     return z;
 }
-__host__ __device__ __forceinline__ uint32_t rng_uniform(uint64_t seed, uint64_t stream, uint64_t counter) {
-    uint64_t z = 0x9E3779B97F4A7C15ull;
-    z = mix64(z ^ seed);
-    z = mix64(z ^ stream);
-    z = mix64(z ^ counter);
-    z = mix64(z);
+// The first two mixing rounds depend only on (seed, stream): rng_key() is
+// hoisted out of element loops, rng_uniform_k() finishes per counter.
+__host__ __device__ __forceinline__ uint64_t rng_key(uint64_t seed, uint64_t stream) {
+    return mix64(mix64(0x9E3779B97F4A7C15ull ^ seed) ^ stream);
+}
+__host__ __device__ __forceinline__ uint32_t rng_uniform_k(uint64_t key, uint64_t counter) {
+    const uint64_t z = mix64(mix64(key ^ counter));
     return (uint32_t)(z >> 32) ^ (uint32_t)z;
+}
+__host__ __device__ __forceinline__ uint32_t rng_uniform(uint64_t seed, uint64_t stream, uint64_t counter) {
+    return rng_uniform_k(rng_key(seed, stream), counter);
 }
 // Returns the f32 bit pattern of SR_bf16(x); representable inputs (and NaN)
 // pass through unchanged.
-__device__ __forceinline__ float sr_bf16(float x, uint64_t seed, uint64_t stream, uint64_t counter) {
+__device__ __forceinline__ float sr_bf16k(float x, uint64_t key, uint64_t counter) {
     uint32_t bits = __float_as_uint(x);
     if ((bits & 0xFFFFu) == 0u || x != x) return x;
-    bits += rng_uniform(seed, stream, counter) & 0xFFFFu;
+    bits += rng_uniform_k(key, counter) & 0xFFFFu;
     bits &= 0xFFFF0000u;
     return __uint_as_float(bits);
 }
+__device__ __forceinline__ float sr_bf16(float x, uint64_t seed, uint64_t stream, uint64_t counter) {
+    return sr_bf16k(x, rng_key(seed, stream), counter);
+}
+
+// n / d and n % d for 0 <= n < 2^31 by multiply-high (d fixed per launch)
+struct FastDiv {
+    uint32_t d, m, l;
+    __host__ FastDiv() : d(1), m(0), l(0) {}
+    __host__ explicit FastDiv(uint32_t dv) : d(dv) {
+        l = 0;
+        while ((1ull << l) < dv) ++l;
+        m = (uint32_t)((((1ull << l) - dv) << 32) / dv + 1);
+    }
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (l == 0) return n;
+        const uint32_t t = __umulhi(n, m);
+        return (t + ((n - t) >> 1)) >> (l - 1);
+    }
+};
 
 // ---------------------------------------------------------------------------
 // absmax as an order-free u32 max of |x| bit patterns: NaN (0x7FC..) > inf >

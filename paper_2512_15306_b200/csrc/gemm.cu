@@ -147,15 +147,16 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
     } else {  // *_ACC: GradAccumulator::accumulate fused (src/model.cpp:455-462)
         uint16_t* buf = reinterpret_cast<uint16_t*>(p.out) + (int64_t)row * p.ldo + col0;
         const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
+        const uint64_t key = rng_key(p.sr_seed, p.sr_stream);
         if (vec) {
             float b[32];
             load_bf16x32(buf, b);
 #pragma unroll
-            for (int j = 0; j < 32; ++j) b[j] = sr_bf16(__fadd_rn(b[j], v[j]), p.sr_seed, p.sr_stream, ctr0 + j);
+            for (int j = 0; j < 32; ++j) b[j] = sr_bf16k(__fadd_rn(b[j], v[j]), key, ctr0 + j);
             store_bf16x32(buf, b);
         } else {
             for (int j = 0; j < 32 && col0 + j < p.N; ++j)
-                buf[j] = f2bfbits(sr_bf16(__fadd_rn(bfbits2f(buf[j]), v[j]), p.sr_seed, p.sr_stream, ctr0 + j));
+                buf[j] = f2bfbits(sr_bf16k(__fadd_rn(bfbits2f(buf[j]), v[j]), key, ctr0 + j));
         }
     }
 }
@@ -380,7 +381,9 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
 // split-K reduction: sum the S f32 partial tiles in split order (fixed, so the
 // result is deterministic) and apply the requested epilogue
 // ---------------------------------------------------------------------------
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int M, int N, int epi,
+// Sums the split-K partials in split order and applies the epilogue; 4 columns
+// per thread (N % 4 == 0, checked by the launcher), rows/cols by FastDiv.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int M, int N, FastDiv n4div, int epi,
                                      const float* __restrict__ a_scale, const float* __restrict__ b_scale,
                                      void* __restrict__ out, int64_t ldo, const uint16_t* __restrict__ res,
                                      int64_t ldr, uint64_t seed, uint64_t stream, uint64_t base) {
@@ -388,28 +391,39 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int M,
     if (a_scale && b_scale) denom = __fmul_rn(*a_scale, *b_scale);
     const float rcp = __frcp_rn(denom);
     const int64_t total = (int64_t)M * N;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        float acc = ws[i];
-        for (int s = 1; s < S; ++s) acc = __fadd_rn(acc, ws[(int64_t)s * total + i]);
-        const int64_t r = i / N, c = i % N;
+    const uint32_t n4 = (uint32_t)(N / 4), tot4 = (uint32_t)(total / 4);
+    const uint64_t key = rng_key(seed, stream);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < tot4; i += gridDim.x * blockDim.x) {
+        float4 acc = reinterpret_cast<const float4*>(ws)[i];
+        for (int sp = 1; sp < S; ++sp) {
+            const float4 w = reinterpret_cast<const float4*>(ws + (int64_t)sp * total)[i];
+            acc.x = __fadd_rn(acc.x, w.x);
+            acc.y = __fadd_rn(acc.y, w.y);
+            acc.z = __fadd_rn(acc.z, w.z);
+            acc.w = __fadd_rn(acc.w, w.w);
+        }
+        const uint32_t r = n4div.div(i), c = (i - r * n4) * 4;
+        const float a[4] = {acc.x, acc.y, acc.z, acc.w};
         if (epi == EPI_F32) {
-            reinterpret_cast<float*>(out)[r * ldo + c] = acc;
+            *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + r * ldo + c) = acc;
             continue;
         }
-        if (epi == EPI_F32_ACC) {
-            uint16_t* b = reinterpret_cast<uint16_t*>(out) + r * ldo + c;
-            *b = f2bfbits(sr_bf16(__fadd_rn(bfbits2f(*b), acc), seed, stream, base + (uint64_t)(r * N + c)));
-            continue;
-        }
-        const float v = bf16r(div_exact(acc, denom, rcp));
         uint16_t* o = reinterpret_cast<uint16_t*>(out) + r * ldo + c;
-        if (epi == EPI_BF16) {
-            *o = f2bfbits(v);
-        } else if (epi == EPI_BF16_RES) {
-            *o = f2bfbits(__fadd_rn(v, bfbits2f(res[r * ldr + c])));
-        } else {  // EPI_BF16_ACC
-            *o = f2bfbits(sr_bf16(__fadd_rn(bfbits2f(*o), v), seed, stream, base + (uint64_t)(r * N + c)));
+        const uint64_t ctr = base + (uint64_t)r * (uint64_t)N + c;
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (epi == EPI_F32_ACC) {
+                v[j] = sr_bf16k(__fadd_rn(bfbits2f(o[j]), a[j]), key, ctr + j);
+                continue;
+            }
+            v[j] = bf16r(div_exact(a[j], denom, rcp));
+            if (epi == EPI_BF16_RES)
+                v[j] = __fadd_rn(v[j], bfbits2f(res[r * ldr + c + j]));
+            else if (epi == EPI_BF16_ACC)
+                v[j] = sr_bf16k(__fadd_rn(bfbits2f(o[j]), v[j]), key, ctr + j);
         }
+        *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
     }
 }
 
@@ -653,7 +667,9 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     p.sr_base = g->sr_base;
     const int tiles = p.num_m * p.num_n;
     int splits = 1;
-    if (g->ws && g->split_k != 1) {
+    // the reduce pass works on 4-column vectors with 32-bit indices
+    const bool reducible = g->N % 4 == 0 && g->ldo % 4 == 0 && g->M * g->N / 4 < (int64_t(1) << 31);
+    if (g->ws && g->split_k != 1 && reducible) {
         splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn, cg);
         if ((int64_t)splits * g->M * g->N * 4 > g->ws_bytes) splits = 1;
     }
@@ -668,8 +684,9 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         int rc2 = dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, EPI_F32, p, grid, cg, s);
         if (rc2) return rc2;
         const int64_t total = g->M * g->N;
-        const int rg = (int)std::min<int64_t>(ceil_div(total, 256), 8 * num_sms());
-        splitk_reduce_kernel<<<rg, 256, 0, s>>>((const float*)g->ws, p.splits, (int)g->M, (int)g->N, g->epi,
+        const int rg = (int)std::min<int64_t>(ceil_div(total / 4, 256), 8 * num_sms());
+        splitk_reduce_kernel<<<rg, 256, 0, s>>>((const float*)g->ws, p.splits, (int)g->M, (int)g->N,
+                                                FastDiv((uint32_t)(g->N / 4)), g->epi,
                                                 g->a_scale, g->b_scale, g->out, g->ldo,
                                                 reinterpret_cast<const uint16_t*>(g->res), g->ldr, g->sr_seed,
                                                 g->sr_stream, g->sr_base);

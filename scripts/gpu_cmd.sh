@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests/test_gemm_gpu.py tests/test_fused_gpu.py -x -q --timeout=60 --timeout-method=thread 2>&1 | tail -3
-timeout 300 python scripts/gemm_bench.py 2>&1 | tail -20
-timeout 120 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"tc_kernel" -c 3 --csv python scripts/attn_big.py 2>/dev/null | grep -E "kernel" | awk -F'","' '{print $5, $NF}' | cut -c1-40,130-
+timeout 900 python -m pytest tests/ -x -q -m gpu --timeout=120 --timeout-method=thread 2>&1 | tail -5
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['mfu']); print(json.dumps(d['kernel_classes']))"
+bash scripts/ncu_launches.sh 2>&1 | head -40

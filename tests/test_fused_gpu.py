@@ -168,10 +168,14 @@ def test_rope_bitexact(ops, ref, rows, T, H, hd):
             want[:, h * hd + half:(h + 1) * hd] = bf16_grid_round((a * s + b * cs).astype(np.float32))
         xt = _bf16(x)
         from paper_2512_15306_b200 import _lib
-        rc = _lib.lib().qtk_rope(xt.data_ptr(), rows, T, H + Hkv, hd, q, tab.data_ptr(), bwd, None,
-                                 torch.cuda.current_stream().cuda_stream)
+        am = torch.zeros(1, dtype=torch.int32, device="cuda")
+        rc = _lib.lib().qtk_rope(xt.data_ptr(), rows, T, H + Hkv, hd, q, tab.data_ptr(), bwd,
+                                 am.data_ptr() if bwd else None, torch.cuda.current_stream().cuda_stream)
         assert rc == 0
         np.testing.assert_array_equal(_np(xt), want)
+        if bwd:  # absmax over the whole row, v columns included
+            want_am = np.abs(bf16_grid_round(want)).max()
+            assert am.view(torch.float32).item() == want_am
 
 
 @pytest.mark.parametrize("N,d,V", [(128, 128, 256), (300, 256, 1000), (64, 896, 4096)])
