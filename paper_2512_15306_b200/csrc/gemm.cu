@@ -39,6 +39,10 @@ struct alignas(64) Params {
     CUtensorMap ta;
     CUtensorMap tb;
     CUtensorMap ta2;  // split-A: D = A.B + A2.B (the K loop runs twice, B repeats)
+    CUtensorMap to;   // output (and EPI_*_ACC accumulator) map, 128-B x 32-row boxes
+    CUtensorMap tr;   // EPI_BF16_RES residual map
+    int tma_out;      // epilogue stages tiles through smem and stores them with TMA
+    int n_fast;       // tile order: N-tiles of one M panel adjacent (they share the A panel in L2)
     int M, N, K;
     int num_m, num_n, num_k;
     int split_a;
@@ -64,9 +68,11 @@ struct Cfg {
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BYTES = BN_CTA * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+    static constexpr int EPI_BYTES = 4 * 2 * 4096;  // per epilogue warp: two 32-row x 128-B staging boxes
+    static constexpr int STAGE_BUDGET = 224 * 1024 - EPI_BYTES - 2048;
+    static constexpr int STAGES = STAGE_BUDGET / STAGE > 8 ? 8 : STAGE_BUDGET / STAGE;
     static constexpr int TMEM_COLS = 2 * BN;
-    static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+    static constexpr int SMEM = STAGES * STAGE + EPI_BYTES + 1024 + 256;
 };
 
 __device__ __forceinline__ void store_bf16x32(uint16_t* dst, const float (&v)[32]) {
@@ -161,6 +167,97 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
     }
 }
 
+// ---------------------------------------------------------------------------
+// Staged epilogue: one 128-B column group (64 bf16 or 32 f32 output columns) of
+// this warp's 32 rows at a time: TMEM -> registers -> rounding -> 128-B-swizzled
+// smem box (lane = row, 16-B chunk c at c ^ (row & 7): conflict-free) -> TMA
+// store.  Two boxes per warp alternate so the store of one overlaps the next
+// group's math.  EPI_BF16_RES / *_ACC first TMA-load the residual / the grad
+// accumulator box into the same smem (zero-filled out of bounds; the store clips).
+// ---------------------------------------------------------------------------
+template <int EPI>
+__device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem_cols, int m_row0, int n0, int BNt,
+                                                  float denom, float rcp, uint8_t* stg, uint64_t* ebar,
+                                                  uint32_t& ephase, int& buf) {
+    constexpr bool F32OUT = EPI == EPI_F32;
+    constexpr int GC = F32OUT ? 32 : 64;  // output columns per 128-B group
+    constexpr bool LOADS = EPI == EPI_BF16_RES || EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC;
+    const int lane = threadIdx.x & 31;
+    const int row = m_row0 + lane;
+    const uint64_t key = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) ? rng_key(p.sr_seed, p.sr_stream) : 0;
+    for (int g = 0; g < BNt / GC; ++g) {
+        const int col0 = n0 + g * GC;
+        if (col0 >= p.N) break;
+        uint32_t r[GC];
+        tmem_ld32(tmem_cols + g * GC, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
+        if constexpr (GC == 64) tmem_ld32(tmem_cols + g * GC + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
+        uint8_t* box = stg + buf * 4096;
+        // the store issued from this box two groups ago must have finished reading it
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if constexpr (LOADS) {
+            if (lane == 0) {
+                mbar_arrive_expect_tx(ebar, 4096);
+                tma_load_2d(EPI == EPI_BF16_RES ? &p.tr : &p.to, ebar, box, col0, m_row0);
+            }
+        }
+        tmem_ld_wait();
+        float v[GC];
+        if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
+#pragma unroll
+            for (int j = 0; j < GC; ++j) v[j] = __uint_as_float(r[j]);
+        } else if constexpr (EPI == EPI_BF16) {
+#pragma unroll
+            for (int j = 0; j < GC; ++j) v[j] = div_exact(__uint_as_float(r[j]), denom, rcp);  // rounded by the pack
+        } else {
+#pragma unroll
+            for (int j = 0; j < GC; ++j) v[j] = bf16r(div_exact(__uint_as_float(r[j]), denom, rcp));
+        }
+        uint4* rowp = reinterpret_cast<uint4*>(box + lane * 128);
+        if constexpr (LOADS) {
+            mbar_wait(ebar, ephase);
+            ephase ^= 1;
+            const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const uint4 u = rowp[c ^ (lane & 7)];
+                const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int j = c * 8 + 2 * e;
+                    const float in0 = __uint_as_float(w[e] << 16), in1 = __uint_as_float(w[e] & 0xFFFF0000u);
+                    if constexpr (EPI == EPI_BF16_RES) {
+                        v[j] = __fadd_rn(v[j], in0);
+                        v[j + 1] = __fadd_rn(v[j + 1], in1);
+                    } else {
+                        v[j] = sr_bf16k(__fadd_rn(in0, v[j]), key, ctr0 + j);
+                        v[j + 1] = sr_bf16k(__fadd_rn(in1, v[j + 1]), key, ctr0 + j + 1);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            uint4 u;
+            if constexpr (F32OUT) {
+                u = make_uint4(__float_as_uint(v[4 * c]), __float_as_uint(v[4 * c + 1]), __float_as_uint(v[4 * c + 2]),
+                               __float_as_uint(v[4 * c + 3]));
+            } else {
+                u = make_uint4(pack_bf16x2(v[8 * c], v[8 * c + 1]), pack_bf16x2(v[8 * c + 2], v[8 * c + 3]),
+                               pack_bf16x2(v[8 * c + 4], v[8 * c + 5]), pack_bf16x2(v[8 * c + 6], v[8 * c + 7]));
+            }
+            rowp[c ^ (lane & 7)] = u;
+        }
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_2d(&p.to, box, col0, m_row0);
+            bulk_commit();
+        }
+        buf ^= 1;
+    }
+}
+
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -180,11 +277,13 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     using C = Cfg<KIND, BN, CG>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + C::STAGES * C::STAGE);
+    uint8_t* stg_base = base + C::STAGES * C::STAGE;  // epilogue staging boxes
+    uint64_t* full = reinterpret_cast<uint64_t*>(stg_base + C::EPI_BYTES);
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* ebar = tempty + 2;  // [4] epilogue TMA-load barriers
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(ebar + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = CG == 2 ? cluster_rank() : 0;
@@ -203,6 +302,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 4 * CG);
         }
+        for (int w = 0; w < 4; ++w) mbar_init(&ebar[w], 1);
         fence_barrier_init();
         fence_async_shared();
     }
@@ -231,8 +331,9 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         uint32_t phase = 0;
         for (int tt = cid; tt < all_tiles; tt += ncl) {
             const int t = tt % tiles, sp = tt / tiles;
-            const int m0 = (t % p.num_m) * BM * CG + (int)crank * BM;
-            const int n0 = (t / p.num_m) * BN + (int)crank * C::BN_CTA;
+            const int tm = p.n_fast ? t / p.num_n : t % p.num_m, tn = p.n_fast ? t % p.num_n : t / p.num_m;
+            const int m0 = tm * BM * CG + (int)crank * BM;
+            const int n0 = tn * BN + (int)crank * C::BN_CTA;
             const int kb0 = sp * p.kb_per_split, kb1 = min(p.num_k, kb0 + p.kb_per_split);
             const int kn = kb1 - kb0;
             const int kiters = p.split_a ? 2 * kn : kn;
@@ -337,6 +438,8 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         float denom = 1.0f;
         if (p.a_scale && p.b_scale) denom = __fmul_rn(*p.a_scale, *p.b_scale);
         const float rcp = __frcp_rn(denom);
+        uint32_t ephase = 0;
+        int ebuf = 0;
         int it = 0;
         for (int tt = cid; tt < all_tiles; tt += ncl, ++it) {
             const int t = tt % tiles, sp = tt / tiles;
@@ -344,14 +447,21 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             const uint32_t aphase = (it >> 1) & 1;
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
-            const int m0 = (t % p.num_m) * BM * CG + (int)crank * BM, n0 = (t / p.num_m) * BN;
-            const int row = m0 + wq * 32 + lane + sp * p.M;  // split partials stack along rows
+            const int tm = p.n_fast ? t / p.num_n : t % p.num_m, tn = p.n_fast ? t % p.num_n : t / p.num_m;
+            const int m0 = tm * BM * CG + (int)crank * BM, n0 = tn * BN;
+            const uint32_t tcols = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN);
+            if (p.tma_out) {
+                epilogue_tile_tma<EPI>(p, tcols, m0 + wq * 32, n0, BN, denom, rcp, stg_base + wq * 8192, &ebar[wq],
+                                       ephase, ebuf);
+            } else {
+                const int row = m0 + wq * 32 + lane + sp * p.M;  // split partials stack along rows
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                tmem_ld32(tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + c * 32), r);
-                tmem_ld_wait();
-                if (row - sp * p.M < p.M) epilogue_chunk<EPI>(p, row, n0 + c * 32, denom, rcp, r);
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tcols + c * 32, r);
+                    tmem_ld_wait();
+                    if (row - sp * p.M < p.M) epilogue_chunk<EPI>(p, row, n0 + c * 32, denom, rcp, r);
+                }
             }
             tc_fence_before();
             __syncwarp();
@@ -364,6 +474,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
                 }
             }
         }
+        if (p.tma_out && lane == 0) bulk_wait<0>();  // staged stores done before the CTA's smem goes away
     }
     __syncthreads();
     if constexpr (CG == 2) cluster_sync_all();
@@ -448,7 +559,9 @@ int make_tmap(CUtensorMap* m, const void* ptr, int elem, uint64_t inner, uint64_
               uint32_t box_inner, uint32_t box_outer) {
     auto fn = encode_fn();
     if (!fn) return 900;
-    const CUtensorMapDataType dt = elem == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    const CUtensorMapDataType dt = elem == 1   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                  : elem == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     cuuint64_t dims[2] = {inner, outer};
     cuuint64_t strides[1] = {row_stride_elems * (uint64_t)elem};
     cuuint32_t box[2] = {box_inner, box_outer};
@@ -691,6 +804,24 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
                                                 reinterpret_cast<const uint16_t*>(g->res), g->ldr, g->sr_seed,
                                                 g->sr_stream, g->sr_base);
         return (int)cudaGetLastError();
+    }
+    // L2-aware order: when an M panel is shared by few N tiles, run those N tiles side by side
+    p.n_fast = p.num_n <= p.num_m;
+    // staged TMA-store epilogue: 16-B aligned output (and residual) rows
+    {
+        const int oel = g->epi == EPI_F32 ? 4 : 2;
+        static int no_tma = -1;
+        if (no_tma < 0) {
+            const char* e = getenv("QTB_GEMM_NO_TMA_EPI");
+            no_tma = e ? atoi(e) : 0;
+        }
+        bool ok = !no_tma && !(reinterpret_cast<uintptr_t>(g->out) & 15) && ((g->ldo * oel) & 15) == 0 &&
+                  g->ldo >= g->N;
+        if (ok && g->epi == EPI_BF16_RES)
+            ok = g->res && !(reinterpret_cast<uintptr_t>(g->res) & 15) && ((g->ldr * 2) & 15) == 0 && g->ldr >= g->N;
+        if (ok) ok = make_tmap(&p.to, g->out, oel, g->N, g->M, g->ldo, 128 / oel, 32) == 0;
+        if (ok && g->epi == EPI_BF16_RES) ok = make_tmap(&p.tr, g->res, 2, g->N, g->M, g->ldr, 64, 32) == 0;
+        p.tma_out = ok ? 1 : 0;
     }
     const int grid = std::min(tiles, num_sms() / cg) * cg;
     return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, cg, s);
