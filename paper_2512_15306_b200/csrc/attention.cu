@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(128) bwd_dq_kernel(const uint16_t* __restrict_
 using namespace qtb;
 using namespace qtb::attn;
 
-static int g_fast_exp = 0, g_bwd_split = 1;
+static int g_fast_exp = 1, g_bwd_split = 1;  // ex2.approx: same parity as expf (scripts/attn_modes.py)
 
 extern "C" {
 

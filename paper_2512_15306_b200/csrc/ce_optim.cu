@@ -254,6 +254,60 @@ __device__ __forceinline__ void store8_bf16(uint16_t* p, const float (&x)[8]) {
                                               pack_bf16x2(x[4], x[5]), pack_bf16x2(x[6], x[7]));
 }
 
+// x / c for a per-launch constant c from rc = RN(1/c): q = RN(x*rc) is within
+// 1 ulp, the FMA residual is exact and one correction gives the correctly
+// rounded quotient (Markstein) -- bitwise __fdiv_rn(x, c) in 3 instructions.
+// Tiny |x| (residual could leave the normal range) takes the IEEE division.
+__device__ __forceinline__ float div_const(float x, float c, float rc) {
+    if (fabsf(x) < 1.0e-30f) return __fdiv_rn(x, c);
+    const float q = __fmul_rn(x, rc);
+    return __fmaf_rn(__fmaf_rn(-q, c, x), rc, q);
+}
+
+struct AdamConst {
+    float b1, b2, omb1, omb2, bc1, bc2, rbc1, rbc2, eps, wd, lr, gscale;
+    uint64_t km, kv, kw;
+    int bf16_moments;
+};
+
+// one element of src/optim.cpp:37-59; returns false for a non-finite gradient
+__device__ __forceinline__ bool adam_elem(const AdamConst& c, float g, float& p, float& m, float& v, uint64_t ctr) {
+    const float gi = __fmul_rn(g, c.gscale);
+    const float m_new = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, gi));
+    const float v_new = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(__fmul_rn(c.omb2, gi), gi));
+    const float mhat = div_const(m_new, c.bc1, c.rbc1);
+    const float vhat = div_const(v_new, c.bc2, c.rbc2);
+    const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), c.eps)), __fmul_rn(c.wd, p));
+    const float p_new = __fsub_rn(p, __fmul_rn(c.lr, upd));
+    if (c.bf16_moments) {
+        m = sr_bf16k(m_new, c.km, ctr);
+        v = sr_bf16k(v_new, c.kv, ctr);
+    } else {
+        m = m_new;
+        v = v_new;
+    }
+    p = sr_bf16k(p_new, c.kw, ctr);
+    return isfinite(gi);
+}
+
+template <typename G>
+__device__ __forceinline__ float4 ld4g(const G* g, int64_t i);
+template <>
+__device__ __forceinline__ float4 ld4g<uint16_t>(const uint16_t* g, int64_t i) {
+    const uint2 u = *reinterpret_cast<const uint2*>(g + i);
+    return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                       __uint_as_float(u.y & 0xFFFF0000u));
+}
+template <>
+__device__ __forceinline__ float4 ld4g<float>(const float* g, int64_t i) {
+    return *reinterpret_cast<const float4*>(g + i);
+}
+__device__ __forceinline__ void st4bf(uint16_t* p, int64_t i, float4 x) {
+    *reinterpret_cast<uint2*>(p + i) = make_uint2(pack_bf16x2(x.x, x.y), pack_bf16x2(x.z, x.w));
+}
+
+// Lane t of the CTA owns 4 consecutive elements per iteration, so a warp
+// touches 128 consecutive elements of every stream (coalesced 8/16-B accesses).
 template <typename G>
 __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p, float* __restrict__ m,
                                                        float* __restrict__ v, uint16_t* __restrict__ m16,
@@ -263,74 +317,76 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
                                                        int* __restrict__ err, uint32_t* __restrict__ seg_amax) {
     const AdamChunk ch = chunks[blockIdx.x];
     const Seg sg = segs[ch.seg];
-    const float one_m_b1 = __fsub_rn(1.0f, h.b1), one_m_b2 = __fsub_rn(1.0f, h.b2);
-    const float gscale = *h.grad_scale;
+    AdamConst c;
+    c.b1 = h.b1;
+    c.b2 = h.b2;
+    c.omb1 = __fsub_rn(1.0f, h.b1);
+    c.omb2 = __fsub_rn(1.0f, h.b2);
+    c.bc1 = h.bc1;
+    c.bc2 = h.bc2;
+    c.rbc1 = __frcp_rn(h.bc1);
+    c.rbc2 = __frcp_rn(h.bc2);
+    c.eps = h.eps;
+    c.wd = h.wd;
+    c.lr = h.lr;
+    c.gscale = *h.grad_scale;
+    c.kw = rng_key(h.seed, sg.sw);
+    c.km = h.bf16_moments ? rng_key(h.seed, sg.sm) : 0;
+    c.kv = h.bf16_moments ? rng_key(h.seed, sg.sv) : 0;
+    c.bf16_moments = h.bf16_moments;
     const int64_t end = min(sg.n, ch.start + (int64_t)ADAM_CHUNK);
-    const uint64_t kw = rng_key(h.seed, sg.sw);
-    const uint64_t km = h.bf16_moments ? rng_key(h.seed, sg.sm) : 0, kv = h.bf16_moments ? rng_key(h.seed, sg.sv) : 0;
+    const uint64_t ctr_base = (uint64_t)(h.step - 1) * (uint64_t)sg.gnumel + (uint64_t)sg.gstart;
+    const bool vec_ok = ((sg.off | sg.poff) & 3) == 0;
+    G const* gs = grad + sg.off;
+    uint16_t* ps = p + sg.poff;
     uint32_t amax = 0;
-    bool bad = false;
-    for (int64_t j0 = ch.start + threadIdx.x * 8; j0 < end; j0 += ADAM_T * 8) {
-        const int64_t i = sg.off + j0;      // moment / grad index
-        const int64_t pi = sg.poff + j0;    // parameter index
-        const int cnt = (int)min((int64_t)8, end - j0);
-        float gv[8], pv[8], mv[8], vv[8];
-        load8<G>(grad, i, sg.off + end, gv);
-        load8<uint16_t>(p, pi, sg.poff + end, pv);
-        if (h.bf16_moments) {
-            load8<uint16_t>(m16, i, sg.off + end, mv);
-            load8<uint16_t>(v16, i, sg.off + end, vv);
-        } else {
-            load8<float>(m, i, sg.off + end, mv);
-            load8<float>(v, i, sg.off + end, vv);
-        }
-        const uint64_t ctr0 = (uint64_t)(h.step - 1) * (uint64_t)sg.gnumel + (uint64_t)(sg.gstart + j0);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            if (k >= cnt) break;
-            const float gi = __fmul_rn(gv[k], gscale);
-            if (!isfinite(gi)) bad = true;
-            const float m_new = __fadd_rn(__fmul_rn(h.b1, mv[k]), __fmul_rn(one_m_b1, gi));
-            const float v_new = __fadd_rn(__fmul_rn(h.b2, vv[k]), __fmul_rn(__fmul_rn(one_m_b2, gi), gi));
-            const float mhat = __fdiv_rn(m_new, h.bc1);
-            const float vhat = __fdiv_rn(v_new, h.bc2);
-            const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), h.eps)), __fmul_rn(h.wd, pv[k]));
-            const float p_new = __fsub_rn(pv[k], __fmul_rn(h.lr, upd));
+    bool ok = true;
+    for (int64_t j = ch.start + threadIdx.x * 4; j < end; j += ADAM_T * 4) {
+        const uint64_t ctr = ctr_base + (uint64_t)j;
+        if (vec_ok && j + 4 <= end) {
+            const float4 g4 = ld4g<G>(gs, j);
+            float4 p4 = ld4g<uint16_t>(ps, j);
+            float4 m4, v4;
             if (h.bf16_moments) {
-                mv[k] = sr_bf16k(m_new, km, ctr0 + k);
-                vv[k] = sr_bf16k(v_new, kv, ctr0 + k);
+                m4 = ld4g<uint16_t>(m16 + sg.off, j);
+                v4 = ld4g<uint16_t>(v16 + sg.off, j);
             } else {
-                mv[k] = m_new;
-                vv[k] = v_new;
+                m4 = *reinterpret_cast<const float4*>(m + sg.off + j);
+                v4 = *reinterpret_cast<const float4*>(v + sg.off + j);
             }
-            pv[k] = sr_bf16k(p_new, kw, ctr0 + k);
-            amax = max(amax, abs_bits(pv[k]));
-        }
-        if (cnt == 8 && (pi & 7) == 0 && (i & 7) == 0) {
-            store8_bf16(p + pi, pv);
+            ok &= adam_elem(c, g4.x, p4.x, m4.x, v4.x, ctr);
+            ok &= adam_elem(c, g4.y, p4.y, m4.y, v4.y, ctr + 1);
+            ok &= adam_elem(c, g4.z, p4.z, m4.z, v4.z, ctr + 2);
+            ok &= adam_elem(c, g4.w, p4.w, m4.w, v4.w, ctr + 3);
+            amax = max(max(max(amax, abs_bits(p4.x)), abs_bits(p4.y)), max(abs_bits(p4.z), abs_bits(p4.w)));
+            st4bf(ps, j, p4);
             if (h.bf16_moments) {
-                store8_bf16(m16 + i, mv);
-                store8_bf16(v16 + i, vv);
+                st4bf(m16 + sg.off, j, m4);
+                st4bf(v16 + sg.off, j, v4);
             } else {
-                *reinterpret_cast<float4*>(m + i) = make_float4(mv[0], mv[1], mv[2], mv[3]);
-                *reinterpret_cast<float4*>(m + i + 4) = make_float4(mv[4], mv[5], mv[6], mv[7]);
-                *reinterpret_cast<float4*>(v + i) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-                *reinterpret_cast<float4*>(v + i + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+                *reinterpret_cast<float4*>(m + sg.off + j) = m4;
+                *reinterpret_cast<float4*>(v + sg.off + j) = v4;
             }
         } else {
-            for (int k = 0; k < cnt; ++k) {
-                p[pi + k] = f2bfbits(pv[k]);
+            for (int64_t e = j; e < min(j + 4, end); ++e) {
+                const int64_t i = sg.off + e;
+                float pe = bfbits2f(ps[e]);
+                float me = h.bf16_moments ? bfbits2f(m16[i]) : m[i];
+                float ve = h.bf16_moments ? bfbits2f(v16[i]) : v[i];
+                ok &= adam_elem(c, gval<G>(gs, e), pe, me, ve, ctr_base + (uint64_t)e);
+                amax = max(amax, abs_bits(pe));
+                ps[e] = f2bfbits(pe);
                 if (h.bf16_moments) {
-                    m16[i + k] = f2bfbits(mv[k]);
-                    v16[i + k] = f2bfbits(vv[k]);
+                    m16[i] = f2bfbits(me);
+                    v16[i] = f2bfbits(ve);
                 } else {
-                    m[i + k] = mv[k];
-                    v[i + k] = vv[k];
+                    m[i] = me;
+                    v[i] = ve;
                 }
             }
         }
     }
-    if (bad) atomicExch(err, 3);  // adamw_step: non-finite gradient (src/optim.cpp:47)
+    if (!ok) atomicExch(err, 3);  // adamw_step: non-finite gradient (src/optim.cpp:47)
     if (seg_amax && amax) atomicMax(&seg_amax[ch.seg], amax);
 }
 
