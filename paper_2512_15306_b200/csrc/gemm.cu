@@ -59,7 +59,9 @@ struct alignas(64) Params {
 
 // CG = CTAs per MMA (tcgen05 cta_group): 2 pairs two SMs on a 256-row tile
 // and splits the B tile between them (half the per-SM operand traffic)
-template <int KIND, int BN, int CG = 1>
+__host__ __device__ constexpr bool epi_loads(int epi) { return epi == EPI_BF16_RES || epi == EPI_BF16_ACC || epi == EPI_F32_ACC; }
+
+template <int KIND, int BN, int CG = 1, int EPI = EPI_BF16>
 struct Cfg {
     static constexpr int ELEM = KIND == 0 ? 1 : 2;
     static constexpr int BK = 128 / ELEM;  // K elements per pipeline stage (one 128-B swizzle row)
@@ -68,8 +70,12 @@ struct Cfg {
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BYTES = BN_CTA * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int EPI_BYTES = 4 * 2 * 4096;  // per epilogue warp: two 32-row x 128-B staging boxes
-    static constexpr int STAGE_BUDGET = 224 * 1024 - EPI_BYTES - 2048;
+    // per epilogue warp: two alternating 32-row x 128-B staging boxes, or -- for
+    // the epilogues that read the output tile first -- the warp's whole 32-row
+    // slice of the tile, prefetched while the tile's MMAs run
+    static constexpr int EPI_GROUPS = epi_loads(EPI) ? BN * 2 / 128 : 2;
+    static constexpr int EPI_BYTES = 4 * EPI_GROUPS * 4096;
+    static constexpr int STAGE_BUDGET = 232448 - 1536 - EPI_BYTES;  // 227 KB opt-in max, less align + barriers
     static constexpr int STAGES = STAGE_BUDGET / STAGE > 8 ? 8 : STAGE_BUDGET / STAGE;
     static constexpr int TMEM_COLS = 2 * BN;
     static constexpr int SMEM = STAGES * STAGE + EPI_BYTES + 1024 + 256;
@@ -175,31 +181,45 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
 // group's math.  EPI_BF16_RES / *_ACC first TMA-load the residual / the grad
 // accumulator box into the same smem (zero-filled out of bounds; the store clips).
 // ---------------------------------------------------------------------------
+// Prefetch (lane 0) of the residual / accumulator slice a LOADS epilogue reads:
+// the warp's 32 rows x BNt columns, one 4-KB box per 64 columns, on ebar.
+template <int EPI>
+__device__ __forceinline__ void epilogue_prefetch(const Params& p, int m_row0, int n0, int BNt, uint8_t* stg,
+                                                  uint64_t* ebar) {
+    bulk_wait_read<0>();  // the previous tile's stores have left these boxes
+    const int ng = min(BNt, p.N - n0 + 63) / 64;
+    mbar_arrive_expect_tx(ebar, ng * 4096);
+    for (int g = 0; g < ng; ++g) tma_load_2d(EPI == EPI_BF16_RES ? &p.tr : &p.to, ebar, stg + g * 4096, n0 + g * 64, m_row0);
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem_cols, int m_row0, int n0, int BNt,
                                                   float denom, float rcp, uint8_t* stg, uint64_t* ebar,
                                                   uint32_t& ephase, int& buf) {
     constexpr bool F32OUT = EPI == EPI_F32;
     constexpr int GC = F32OUT ? 32 : 64;  // output columns per 128-B group
-    constexpr bool LOADS = EPI == EPI_BF16_RES || EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC;
+    constexpr bool LOADS = epi_loads(EPI);
     const int lane = threadIdx.x & 31;
     const int row = m_row0 + lane;
     const uint64_t key = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) ? rng_key(p.sr_seed, p.sr_stream) : 0;
+    if constexpr (LOADS) {
+        mbar_wait(ebar, ephase);
+        ephase ^= 1;
+    }
     for (int g = 0; g < BNt / GC; ++g) {
         const int col0 = n0 + g * GC;
         if (col0 >= p.N) break;
         uint32_t r[GC];
         tmem_ld32(tmem_cols + g * GC, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         if constexpr (GC == 64) tmem_ld32(tmem_cols + g * GC + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
-        uint8_t* box = stg + buf * 4096;
-        // the store issued from this box two groups ago must have finished reading it
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
+        uint8_t* box;
         if constexpr (LOADS) {
-            if (lane == 0) {
-                mbar_arrive_expect_tx(ebar, 4096);
-                tma_load_2d(EPI == EPI_BF16_RES ? &p.tr : &p.to, ebar, box, col0, m_row0);
-            }
+            box = stg + g * 4096;
+        } else {
+            box = stg + buf * 4096;
+            // the store issued from this box two groups ago must have finished reading it
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
         }
         tmem_ld_wait();
         float v[GC];
@@ -215,8 +235,6 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
         }
         uint4* rowp = reinterpret_cast<uint4*>(box + lane * 128);
         if constexpr (LOADS) {
-            mbar_wait(ebar, ephase);
-            ephase ^= 1;
             const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
@@ -274,7 +292,7 @@ __device__ __forceinline__ uint32_t mapa_rank0(uint32_t local) {
 
 template <int KIND, bool A_MN, bool B_MN, int BN, int EPI, int CG>
 __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Params p) {
-    using C = Cfg<KIND, BN, CG>;
+    using C = Cfg<KIND, BN, CG, EPI>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stg_base = base + C::STAGES * C::STAGE;  // epilogue staging boxes
@@ -445,14 +463,17 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             const int t = tt % tiles, sp = tt / tiles;
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
-            mbar_wait(&tfull[acc], aphase);
-            tc_fence_after();
             const int tm = p.n_fast ? t / p.num_n : t % p.num_m, tn = p.n_fast ? t % p.num_n : t / p.num_m;
             const int m0 = tm * BM * CG + (int)crank * BM, n0 = tn * BN;
+            if constexpr (epi_loads(EPI)) {
+                if (p.tma_out && lane == 0) epilogue_prefetch<EPI>(p, m0 + wq * 32, n0, BN, stg_base + wq * C::EPI_GROUPS * 4096, &ebar[wq]);
+            }
+            mbar_wait(&tfull[acc], aphase);
+            tc_fence_after();
             const uint32_t tcols = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN);
             if (p.tma_out) {
-                epilogue_tile_tma<EPI>(p, tcols, m0 + wq * 32, n0, BN, denom, rcp, stg_base + wq * 8192, &ebar[wq],
-                                       ephase, ebuf);
+                epilogue_tile_tma<EPI>(p, tcols, m0 + wq * 32, n0, BN, denom, rcp,
+                                       stg_base + wq * C::EPI_GROUPS * 4096, &ebar[wq], ephase, ebuf);
             } else {
                 const int row = m0 + wq * 32 + lane + sp * p.M;  // split partials stack along rows
 #pragma unroll 1
@@ -576,7 +597,7 @@ using KernelFn = void (*)(Params);
 
 template <int KIND, bool A_MN, bool B_MN, int BN, int EPI, int CG>
 int launch_cg(const Params& p, int grid, cudaStream_t s) {
-    using C = Cfg<KIND, BN, CG>;
+    using C = Cfg<KIND, BN, CG, EPI>;
     // an MN-major operand tile must span whole 128-B swizzle atoms per CTA
     if constexpr (B_MN && (C::BN_CTA * C::ELEM) % 128 != 0) {
         return 903;
