@@ -36,12 +36,12 @@ struct Smem {
     static constexpr int K = BKV * HD * 2;   // one K stage
     static constexpr int V = BKV * HD * 2;   // one V stage
     static constexpr int P = BQ * BKV * 2;   // one P part (hi or lo): 2 atom columns
+    static constexpr int NPB = HD == 64 ? 2 : 1;  // P (hi+lo) buffers: double-buffered when they fit
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + Q;
     static constexpr int OFF_V = OFF_K + 2 * K;
-    static constexpr int OFF_PH = OFF_V + 2 * V;
-    static constexpr int OFF_PL = OFF_PH + P;
-    static constexpr int OFF_BAR = OFF_PL + P;
+    static constexpr int OFF_PH = OFF_V + 2 * V;  // buffer b: hi at OFF_PH + 2*b*P, lo at + P
+    static constexpr int OFF_BAR = OFF_PH + 2 * NPB * P;
     static constexpr int BYTES = OFF_BAR + 256 + 4 * BQ * 4 + 1024;  // barriers, (m, l) exchange, align
 };
 
@@ -82,10 +82,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
     uint64_t* v_empty = bar + 7;  // [2]
     uint64_t* s_full = bar + 9;   // [2]
     uint64_t* s_empty = bar + 11; // [2]
-    uint64_t* p_full = bar + 13;
-    uint64_t* p_empty = bar + 14;
-    uint64_t* o_full = bar + 15;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 16);
+    uint64_t* p_full = bar + 13;   // [2]
+    uint64_t* p_empty = bar + 15;  // [2]
+    uint64_t* o_full = bar + 17;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 18);
 
     const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
     const int kvh = h / (H / Hkv);
@@ -105,8 +105,10 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
             mbar_init(&s_full[i], 1);
             mbar_init(&s_empty[i], NSW);
         }
-        mbar_init(p_full, NSW);
-        mbar_init(p_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&p_full[i], NSW);
+            mbar_init(&p_empty[i], 1);
+        }
         mbar_init(o_full, 1);
         fence_barrier_init();
         fence_async_shared();
@@ -167,11 +169,13 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
         issue_s();                                // pass 2, tile 0
         for (int j = 0; j < nj; ++j) {
             if (j + 1 < nj) issue_s();
-            mbar_wait(p_full, j & 1);
+            const int pb = S::NPB == 2 ? (j & 1) : 0;
+            const uint32_t pph = S::NPB == 2 ? ((j >> 1) & 1) : (j & 1);
+            mbar_wait(&p_full[pb], pph);
             mbar_wait(&v_full[vs], vph);
             tc_fence_after();
             const uint32_t va = s_base + S::OFF_V + vs * S::V;
-            const uint32_t ph = s_base + S::OFF_PH, pl = s_base + S::OFF_PL;
+            const uint32_t ph = s_base + S::OFF_PH + pb * 2 * S::P, pl = ph + S::P;
 #pragma unroll
             for (int kk = 0; kk < BKV / 16; ++kk) {
                 const uint64_t bd = mndesc(va, kk, BKV * 128);
@@ -179,59 +183,68 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
                 mma_bf16_ss(tmem + 256, kdesc(pl, kk, BQ * 128), bd, idesc_o, 1);
             }
             tc_commit(&v_empty[vs]);
-            tc_commit(p_empty);
+            tc_commit(&p_empty[pb]);
             if (++vs == 2) { vs = 0; vph ^= 1; }
         }
         tc_commit(o_full);
     } else if (warp >= 4) {
         // ===== softmax: thread = (query row, key half) =====
+        // Scores stay in raw QK^T units; x = s/sqrt(hd) enters only through
+        // a = log2(e)/sqrt(hd): exp(x - m) = ex2(s*a - m_raw*a) (one FMA).
         const int wq = warp & 3, half = (warp - 4) >> 2;
         const int r = wq * 32 + lane;
         const int q = qt * BQ + r;  // position in the sequence
         const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
         const int c0 = half * (BKV / 2);  // this thread's 64 keys of each tile
-        float* xch = reinterpret_cast<float*>(sm + S::OFF_BAR + 256);  // [2][BQ] (m, l) exchange
-        float m = -INFINITY, l = 0.0f;
+        const float a = inv_sqrt_d * LOG2E;
+        float* xch = reinterpret_cast<float*>(sm + S::OFF_BAR + 256);  // [4][BQ] (m, l) exchange
+        float m = -INFINITY, l = 0.0f;  // m: running max of the raw scores
         int sc = 0;
-        // pass 1: running max / sum over this half's keys (S read twice: max, then sum)
-        for (int j = 0; j < nj; ++j) {
+        // S tile -> 64 registers, and the TMEM buffer handed back at once
+        auto load_s = [&](uint32_t (&rr)[64]) {
             const int sb = sc & 1;
             mbar_wait(&s_full[sb], (sc >> 1) & 1);
             tc_fence_after();
-            const int k0 = j * BKV + c0;
-            float mt = -INFINITY;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t rr[32];
-                tmem_ld32(lane_base + sb * BKV + c0 + c * 32, rr);
-                tmem_ld_wait();
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int key = k0 + c * 32 + i;
-                    if (key <= q && key < T) mt = fmaxf(mt, __uint_as_float(rr[i]) * inv_sqrt_d);
-                }
-            }
-            const float mn = fmaxf(m, mt);
-            if (mn != -INFINITY) {
-                float ssum = 0.0f;
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    uint32_t rr[32];
-                    tmem_ld32(lane_base + sb * BKV + c0 + c * 32, rr);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const int key = k0 + c * 32 + i;
-                        if (key <= q && key < T) ssum += ex2((__uint_as_float(rr[i]) * inv_sqrt_d - mn) * LOG2E);
-                    }
-                }
-                l = (m == -INFINITY ? 0.0f : l * ex2((m - mn) * LOG2E)) + ssum;
-                m = mn;
-            }
+            tmem_ld32(lane_base + sb * BKV + c0, *reinterpret_cast<uint32_t(*)[32]>(&rr[0]));
+            tmem_ld32(lane_base + sb * BKV + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&rr[32]));
+            tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[sb]);
             ++sc;
+        };
+        // keys past the query position exist only in the diagonal tile (BQ == BKV)
+        auto masked = [&](int j, int i) { return j == qt && (j * BKV + c0 + i > q); };
+        // pass 1: running max / sum over this half's keys
+        for (int j = 0; j < nj; ++j) {
+            uint32_t rr[64];
+            load_s(rr);
+            float mt = -INFINITY;
+            if (j == qt) {
+#pragma unroll
+                for (int i = 0; i < 64; ++i)
+                    if (!masked(j, i)) mt = fmaxf(mt, __uint_as_float(rr[i]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 64; ++i) mt = fmaxf(mt, __uint_as_float(rr[i]));
+            }
+            const float mn = fmaxf(m, mt);
+            if (mn != -INFINITY) {
+                const float mb = mn * a;
+                float ssum = 0.0f;
+                if (j == qt) {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        if (!masked(j, i)) ssum += ex2(__fmaf_rn(__uint_as_float(rr[i]), a, -mb));
+                } else {
+                    float s2[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) s2[i & 3] += ex2(__fmaf_rn(__uint_as_float(rr[i]), a, -mb));
+                    ssum = (s2[0] + s2[1]) + (s2[2] + s2[3]);
+                }
+                l = (m == -INFINITY ? 0.0f : l * ex2((m - mn) * a)) + ssum;
+                m = mn;
+            }
         }
         // combine the two halves' (m, l) once
         if (half == 1) {
@@ -244,8 +257,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
             const float mg = fmaxf(m, m1);
             float lg = 0.0f;
             if (mg != -INFINITY) {
-                lg = (m == -INFINITY ? 0.0f : l * ex2((m - mg) * LOG2E)) +
-                     (m1 == -INFINITY ? 0.0f : l1 * ex2((m1 - mg) * LOG2E));
+                lg = (m == -INFINITY ? 0.0f : l * ex2((m - mg) * a)) + (m1 == -INFINITY ? 0.0f : l1 * ex2((m1 - mg) * a));
             }
             xch[2 * BQ + r] = mg;
             xch[3 * BQ + r] = lg;
@@ -254,53 +266,37 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
         m = xch[2 * BQ + r];
         l = xch[3 * BQ + r];
         const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+        const float mb = m * a;
         // pass 2: normalised probabilities -> P hi/lo in SMEM (this half = one atom column)
-        uint8_t* ph = sm + S::OFF_PH + half * BQ * 128;
-        uint8_t* pl = sm + S::OFF_PL + half * BQ * 128;
         for (int j = 0; j < nj; ++j) {
-            const int sb = sc & 1;
-            mbar_wait(&s_full[sb], (sc >> 1) & 1);
-            mbar_wait(p_empty, (j & 1) ^ 1);
-            tc_fence_after();
-            const int k0 = j * BKV + c0;
+            uint32_t rr[64];
+            load_s(rr);
+            const int pb = S::NPB == 2 ? (j & 1) : 0;
+            const uint32_t pph = S::NPB == 2 ? ((j >> 1) & 1) : (j & 1);
+            uint8_t* ph = sm + S::OFF_PH + pb * 2 * S::P + half * BQ * 128;
+            uint8_t* pl = ph + S::P;
+            uint32_t hi[32], lo[32];
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                uint32_t rr[32];
-                tmem_ld32(lane_base + sb * BKV + c0 + c * 32, rr);
-                tmem_ld_wait();
-                uint32_t hi[16], lo[16];
+            for (int i = 0; i < 64; i += 2) {
+                float pp[2];
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    float pp[2];
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int key = k0 + c * 32 + i + e;
-                        const float xv = __uint_as_float(rr[i + e]) * inv_sqrt_d;
-                        pp[e] = (key <= q && key < T) ? ex2((xv - m) * LOG2E) * inv_l : 0.0f;
-                    }
-                    const float h0 = bf16r(pp[0]), h1 = bf16r(pp[1]);
-                    hi[i / 2] = pack_bf16x2(h0, h1);
-                    lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
-                }
-                // K-major SW128: key chunk cc (8 keys) at r*128 + ((cc ^ (r&7)) * 16)
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    const int cc = c * 4 + q4;
-                    const int off = r * 128 + ((cc ^ (r & 7)) << 4);
-                    *reinterpret_cast<uint4*>(ph + off) =
-                        make_uint4(hi[q4 * 4 + 0], hi[q4 * 4 + 1], hi[q4 * 4 + 2], hi[q4 * 4 + 3]);
-                    *reinterpret_cast<uint4*>(pl + off) =
-                        make_uint4(lo[q4 * 4 + 0], lo[q4 * 4 + 1], lo[q4 * 4 + 2], lo[q4 * 4 + 3]);
-                }
+                for (int e = 0; e < 2; ++e)
+                    pp[e] = masked(j, i + e) ? 0.0f : ex2(__fmaf_rn(__uint_as_float(rr[i + e]), a, -mb)) * inv_l;
+                const float h0 = bf16r(pp[0]), h1 = bf16r(pp[1]);
+                hi[i / 2] = pack_bf16x2(h0, h1);
+                lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
             }
-            tc_fence_before();
+            mbar_wait(&p_empty[pb], pph ^ 1);
+            // K-major SW128: key chunk cc (8 keys) at r*128 + ((cc ^ (r&7)) * 16)
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+                const int off = r * 128 + ((cc ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[cc * 4 + 0], hi[cc * 4 + 1], hi[cc * 4 + 2], hi[cc * 4 + 3]);
+                *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[cc * 4 + 0], lo[cc * 4 + 1], lo[cc * 4 + 2], lo[cc * 4 + 3]);
+            }
             fence_async_shared();  // generic-proxy stores -> visible to the tensor core
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&s_empty[sb]);
-                mbar_arrive(p_full);
-            }
-            ++sc;
+            if (lane == 0) mbar_arrive(&p_full[pb]);
         }
         // epilogue: this half's HD/2 columns of the O row -> bf16 att + f32 copy; LSE; absmax
         mbar_wait(o_full, 0);
@@ -334,7 +330,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
                 }
             }
         }
-        if (valid && half == 0) lse[((int64_t)b * H + h) * T + q] = m + logf(l);
+        if (valid && half == 0) lse[((int64_t)b * H + h) * T + q] = m * inv_sqrt_d + logf(l);  // m: raw-score max
         mx = warp_max_u32(mx);
         if (lane == 0 && amax && mx) atomicMax(amax, mx);
     }

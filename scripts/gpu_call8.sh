@@ -1,0 +1,11 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+QTB_ATTN_TC=1 timeout 300 python scripts/attn_modes.py 2>&1 | tail -1
+QTB_ATTN_TC=0 timeout 300 python scripts/attn_modes.py 2>&1 | tail -1
+timeout 1200 python -m pytest tests/ -x -q -m gpu --timeout=300 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --profile-json gpurun_out/bench_profile.json > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
+python -c "
+import json;d=json.load(open('gpurun_out/bench_profile.json'));l=d['line'];print(l['value'],l['ms_per_step'],l['mfu'],l['clocks']);print(json.dumps(l['kernel_classes']))"
+timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python scripts/profile_step.py > gpurun_out/ncu_launch.log 2>&1; echo "ncu rc=$?"
+python scripts/summarize_launches.py gpurun_out/launches.csv 25
