@@ -66,6 +66,9 @@ __global__ void __launch_bounds__(NT) absmax_f32_kernel(const float* __restrict_
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float load_amax(const uint32_t* p) { return __uint_as_float(*p); }
 
+// cast: lane i of the grid converts 8 consecutive bf16 (one 16-B load) to 8
+// codes (one 8-B store) -- a warp moves 512 contiguous bytes in and 256 out;
+// 4 vectors per thread in flight.
 template <int NT>
 __global__ void __launch_bounds__(NT) quantize_bf16_kernel(const uint16_t* __restrict__ x, int64_t n, int kind,
                                                            const uint32_t* __restrict__ amax_bits,
@@ -73,27 +76,36 @@ __global__ void __launch_bounds__(NT) quantize_bf16_kernel(const uint16_t* __res
                                                            float* __restrict__ scale_out) {
     const float scale = absmax_scale(load_amax(amax_bits), kind);
     if (blockIdx.x == 0 && threadIdx.x == 0 && scale_out) *scale_out = scale;
-    const int64_t n16 = n / 16;
+    const int64_t n8 = n / 8;
     const uint4* xv = reinterpret_cast<const uint4*>(x);
-    uint4* cv = reinterpret_cast<uint4*>(codes);
-    for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n16; i += (int64_t)gridDim.x * NT) {
-        const uint4 a = __ldcs(xv + 2 * i), b = __ldcs(xv + 2 * i + 1);
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-        uint32_t o[4];
+    uint2* cv = reinterpret_cast<uint2*>(codes);
+    constexpr int U = 4;
+    const int64_t stride = (int64_t)gridDim.x * NT;
+    for (int64_t i0 = (int64_t)blockIdx.x * NT + threadIdx.x; i0 < n8; i0 += U * stride) {
+        uint4 v[U];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const uint32_t p0 = quant2(__uint_as_float(w[2 * j] << 16), __uint_as_float(w[2 * j] & 0xFFFF0000u),
-                                       scale, kind);
-            const uint32_t p1 = quant2(__uint_as_float(w[2 * j + 1] << 16),
-                                       __uint_as_float(w[2 * j + 1] & 0xFFFF0000u), scale, kind);
-            o[j] = p0 | (p1 << 16);
+        for (int k = 0; k < U; ++k)
+            if (i0 + k * stride < n8) v[k] = __ldcs(xv + i0 + k * stride);
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            if (i0 + k * stride < n8) {
+                const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+                uint32_t o[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const uint32_t p0 = quant2(__uint_as_float(w[2 * j] << 16), __uint_as_float(w[2 * j] & 0xFFFF0000u),
+                                               scale, kind);
+                    const uint32_t p1 = quant2(__uint_as_float(w[2 * j + 1] << 16),
+                                               __uint_as_float(w[2 * j + 1] & 0xFFFF0000u), scale, kind);
+                    o[j] = p0 | (p1 << 16);
+                }
+                cv[i0 + k * stride] = make_uint2(o[0], o[1]);
+            }
         }
-        cv[i] = make_uint4(o[0], o[1], o[2], o[3]);
     }
     // tail
-    for (int64_t i = n16 * 16 + (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+    for (int64_t i = n8 * 8 + (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += stride)
         codes[i] = (uint8_t)(quant2(bfbits2f(x[i]), 0.0f, scale, kind) & 0xFF);
-    }
 }
 
 // transpose cast: x (rows, cols) bf16 -> codes_t (cols, rows); optionally also
@@ -185,7 +197,7 @@ int qtk_absmax_f32(const float* x, int64_t n, uint32_t* amax_bits, cudaStream_t 
 int qtk_quantize_bf16(const void* x, int64_t n, int kind, const uint32_t* amax_bits, uint8_t* codes,
                       float* scale_out, cudaStream_t s) {
     if (n <= 0) return 0;
-    const int64_t want = ceil_div(n / 16 + 1, 256);
+    const int64_t want = ceil_div(n / 32 + 1, 256);  // >= 4 vectors of 8 per thread
     const int grid = (int)(want < 8 * kNumSMs ? want : 8 * kNumSMs);
     quantize_bf16_kernel<256><<<grid, 256, 0, s>>>(reinterpret_cast<const uint16_t*>(x), n, kind, amax_bits, codes,
                                                    scale_out);
