@@ -652,7 +652,7 @@ int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_
         use_tc = e ? atoi(e) : 1;  // tcgen05 forward for hd 64 (QTB_ATTN_TC=0: the mma.sync kernel)
     }
     // tcgen05 path for head_dim 64/128; the mma.sync kernel covers the rest
-    if (use_tc && hd == 64)  // hd 128: P + K/V stages exceed 227 KB of smem
+    if (use_tc && (hd == 64 || hd == 128))
         return qtk_attn_fwd_tc(qkv, B, T, H, Hkv, hd, qkv_dim, out, ldo, out32, lse, amax, s);
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     dim3 grid((unsigned)ceil_div(T, 64), H, B);

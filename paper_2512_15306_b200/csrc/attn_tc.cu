@@ -37,10 +37,11 @@ struct Smem {
     static constexpr int V = BKV * HD * 2;   // one V stage
     static constexpr int P = BQ * BKV * 2;   // one P part (hi or lo): 2 atom columns
     static constexpr int NPB = HD == 64 ? 2 : 1;  // P (hi+lo) buffers: double-buffered when they fit
+    static constexpr int NVS = HD == 64 ? 2 : 1;  // V stages (hd 128: one, to stay within 227 KB)
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = OFF_Q + Q;
     static constexpr int OFF_V = OFF_K + 2 * K;
-    static constexpr int OFF_PH = OFF_V + 2 * V;  // buffer b: hi at OFF_PH + 2*b*P, lo at + P
+    static constexpr int OFF_PH = OFF_V + NVS * V;  // buffer b: hi at OFF_PH + 2*b*P, lo at + P
     static constexpr int OFF_BAR = OFF_PH + 2 * NPB * P;
     static constexpr int BYTES = OFF_BAR + 256 + 4 * BQ * 4 + 1024;  // barriers, (m, l) exchange, align
 };
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
                     for (int c = 0; c < HD / 64; ++c)
                         tma_load_2d(&tm, &v_full[vs], sm + S::OFF_V + vs * S::V + c * BKV * 128,
                                     d + Hkv * HD + kvh * HD + c * 64, krow);
-                    if (++vs == 2) { vs = 0; vph ^= 1; }
+                    if (++vs == S::NVS) { vs = 0; vph ^= 1; }
                 }
             }
         }
@@ -184,7 +185,7 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
             }
             tc_commit(&v_empty[vs]);
             tc_commit(&p_empty[pb]);
-            if (++vs == 2) { vs = 0; vph ^= 1; }
+            if (++vs == S::NVS) { vs = 0; vph ^= 1; }
         }
         tc_commit(o_full);
     } else if (warp >= 4) {

@@ -185,25 +185,41 @@ __device__ __forceinline__ void load8<float>(const float* g, int64_t i, int64_t 
 template <typename G>
 __global__ void norm_partials_kernel(const G* __restrict__ g, const Seg* __restrict__ segs, int nseg, int64_t nblk,
                                      double* __restrict__ part) {
-    const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // segment starts staged once per CTA; warps grid-stride over the blocks and
+    // binary-search shared memory
+    extern __shared__ int64_t s_blk0[];
+    for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_blk0[i] = segs[i].blk0;
+    __syncthreads();
     const int lane = threadIdx.x & 31;
-    if (b >= nblk) return;
-    int lo = 0, hi = nseg - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (segs[mid].blk0 <= b) lo = mid;
-        else hi = mid - 1;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    constexpr int U = 4;  // blocks (16-B loads per lane) in flight per warp
+    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b0 < nblk; b0 += U * nw) {
+        float x[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = b0 + u * nw;
+            if (b < nblk) {
+                int lo = 0, hi = nseg - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_blk0[mid] <= b) lo = mid;
+                    else hi = mid - 1;
+                }
+                load8<G>(g + segs[lo].off, (b - s_blk0[lo]) * 256 + lane * 8, segs[lo].n, x[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t b = b0 + u * nw;
+            if (b >= nblk) break;
+            double p = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) p = __dadd_rn(p, __dmul_rn((double)x[u][j], (double)x[u][j]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, o));
+            if (lane == 0) part[b] = p;
+        }
     }
-    const Seg sg = segs[lo];
-    const int64_t i0 = (b - sg.blk0) * 256 + lane * 8;
-    float x[8];
-    load8<G>(g + sg.off, i0, sg.n, x);
-    double p = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) p = __dadd_rn(p, __dmul_rn((double)x[j], (double)x[j]));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, o));
-    if (lane == 0) part[b] = p;
 }
 
 __global__ void sum_f64_kernel(const double* __restrict__ in, int64_t n, double* __restrict__ out) {
@@ -417,11 +433,11 @@ int qtk_seg_size(void) { return (int)sizeof(Seg); }
 int qtk_grad_sumsq(const void* grad, int grad_f32, const void* segs, int nseg, int64_t nblk, double* partials,
                    double* scratch, double* out, cudaStream_t s) {
     if (nblk <= 0) return cudaMemsetAsync(out, 0, sizeof(double), s);
-    const unsigned g = (unsigned)ceil_div(nblk * 32, 256);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(nblk * 32, 256), 32 * kNumSMs);
     if (grad_f32)
-        norm_partials_kernel<float><<<g, 256, 0, s>>>((const float*)grad, (const Seg*)segs, nseg, nblk, partials);
+        norm_partials_kernel<float><<<g, 256, nseg * sizeof(int64_t), s>>>((const float*)grad, (const Seg*)segs, nseg, nblk, partials);
     else
-        norm_partials_kernel<uint16_t><<<g, 256, 0, s>>>((const uint16_t*)grad, (const Seg*)segs, nseg, nblk, partials);
+        norm_partials_kernel<uint16_t><<<g, 256, nseg * sizeof(int64_t), s>>>((const uint16_t*)grad, (const Seg*)segs, nseg, nblk, partials);
     const int nb = (int)std::min<int64_t>(1024, ceil_div(nblk, 256));
     sum_f64_kernel<<<nb, 256, 0, s>>>(partials, nblk, scratch);
     sum_f64_kernel<<<1, 256, 0, s>>>(scratch, nb, out);
