@@ -70,11 +70,14 @@ struct Cfg {
     static constexpr int A_BYTES = BM * 128;
     static constexpr int B_BYTES = BN_CTA * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    // per epilogue warp: two alternating 32-row x 128-B staging boxes, or -- for
-    // the epilogues that read the output tile first -- the warp's whole 32-row
-    // slice of the tile, prefetched while the tile's MMAs run
-    static constexpr int EPI_GROUPS = epi_loads(EPI) ? BN * 2 / 128 : 2;
-    static constexpr int EPI_BYTES = 4 * EPI_GROUPS * 4096;
+    // per epilogue warp: one 32-row x 128-B staging box, or -- for the
+    // epilogues that read the output tile first -- the warp's whole 32-row
+    // slice of its columns, prefetched while the tile's MMAs run
+    // 8 epilogue warps (two per TMEM lane quarter, each owning half of the
+    // tile's columns); a LOADS warp keeps its whole 32 x BN/2 slice
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int EPI_GROUPS = epi_loads(EPI) ? BN / 128 : 1;
+    static constexpr int EPI_BYTES = EPI_WARPS * EPI_GROUPS * 4096;
     static constexpr int STAGE_BUDGET = 232448 - 1536 - EPI_BYTES;  // 227 KB opt-in max, less align + barriers
     static constexpr int STAGES = STAGE_BUDGET / STAGE > 8 ? 8 : STAGE_BUDGET / STAGE;
     static constexpr int TMEM_COLS = 2 * BN;
@@ -187,7 +190,7 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_prefetch(const Params& p, int m_row0, int n0, int BNt, uint8_t* stg,
                                                   uint64_t* ebar) {
     bulk_wait_read<0>();  // the previous tile's stores have left these boxes
-    const int ng = min(BNt, p.N - n0 + 63) / 64;
+    const int ng = max(0, min(BNt, p.N - n0 + 63)) / 64;  // 0 when this half lies past N
     mbar_arrive_expect_tx(ebar, ng * 4096);
     for (int g = 0; g < ng; ++g) tma_load_2d(EPI == EPI_BF16_RES ? &p.tr : &p.to, ebar, stg + g * 4096, n0 + g * 64, m_row0);
 }
@@ -216,9 +219,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
         if constexpr (LOADS) {
             box = stg + g * 4096;
         } else {
-            box = stg + buf * 4096;
-            // the store issued from this box two groups ago must have finished reading it
-            if (lane == 0) bulk_wait_read<1>();
+            box = stg;
+            // the store issued from this box by the previous group must have finished reading it
+            if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
         }
         tmem_ld_wait();
@@ -290,8 +293,10 @@ __device__ __forceinline__ uint32_t mapa_rank0(uint32_t local) {
     return r;
 }
 
+constexpr int GEMM_THREADS = 384;  // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..11 epilogue
+
 template <int KIND, bool A_MN, bool B_MN, int BN, int EPI, int CG>
-__global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_constant__ Params p) {
     using C = Cfg<KIND, BN, CG, EPI>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -301,7 +306,7 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
     uint64_t* tfull = empty + C::STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* ebar = tempty + 2;  // [4] epilogue TMA-load barriers
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(ebar + 4);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(ebar + C::EPI_WARPS);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t crank = CG == 2 ? cluster_rank() : 0;
@@ -318,9 +323,9 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4 * CG);
+            mbar_init(&tempty[a], C::EPI_WARPS * CG);
         }
-        for (int w = 0; w < 4; ++w) mbar_init(&ebar[w], 1);
+        for (int w = 0; w < C::EPI_WARPS; ++w) mbar_init(&ebar[w], 1);
         fence_barrier_init();
         fence_async_shared();
     }
@@ -452,7 +457,9 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> rounding -> HBM =====
-        const int wq = warp - 4;
+        const int ew = warp - 4, wq = warp & 3, half = ew >> 2;  // TMEM lane quarter = warp % 4
+        constexpr int BNH = BN / 2;                               // this warp's columns of the tile
+        uint8_t* stg = stg_base + ew * C::EPI_GROUPS * 4096;
         float denom = 1.0f;
         if (p.a_scale && p.b_scale) denom = __fmul_rn(*p.a_scale, *p.b_scale);
         const float rcp = __frcp_rn(denom);
@@ -464,20 +471,19 @@ __global__ void __launch_bounds__(256, 1) gemm_kernel(const __grid_constant__ Pa
             const int acc = it & 1;
             const uint32_t aphase = (it >> 1) & 1;
             const int tm = p.n_fast ? t / p.num_n : t % p.num_m, tn = p.n_fast ? t % p.num_n : t / p.num_m;
-            const int m0 = tm * BM * CG + (int)crank * BM, n0 = tn * BN;
+            const int m0 = tm * BM * CG + (int)crank * BM, n0 = tn * BN + half * BNH;
             if constexpr (epi_loads(EPI)) {
-                if (p.tma_out && lane == 0) epilogue_prefetch<EPI>(p, m0 + wq * 32, n0, BN, stg_base + wq * C::EPI_GROUPS * 4096, &ebar[wq]);
+                if (p.tma_out && lane == 0) epilogue_prefetch<EPI>(p, m0 + wq * 32, n0, BNH, stg, &ebar[ew]);
             }
             mbar_wait(&tfull[acc], aphase);
             tc_fence_after();
-            const uint32_t tcols = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN);
+            const uint32_t tcols = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(acc * BN + half * BNH);
             if (p.tma_out) {
-                epilogue_tile_tma<EPI>(p, tcols, m0 + wq * 32, n0, BN, denom, rcp,
-                                       stg_base + wq * C::EPI_GROUPS * 4096, &ebar[wq], ephase, ebuf);
+                epilogue_tile_tma<EPI>(p, tcols, m0 + wq * 32, n0, BNH, denom, rcp, stg, &ebar[ew], ephase, ebuf);
             } else {
                 const int row = m0 + wq * 32 + lane + sp * p.M;  // split partials stack along rows
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = 0; c < BNH / 32; ++c) {
                     uint32_t r[32];
                     tmem_ld32(tcols + c * 32, r);
                     tmem_ld_wait();
@@ -610,11 +616,11 @@ int launch_cg(const Params& p, int grid, cudaStream_t s) {
         attr_set = true;
     }
     if constexpr (CG == 1) {
-        k<<<grid, 256, C::SMEM, s>>>(p);
+        k<<<grid, GEMM_THREADS, C::SMEM, s>>>(p);
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(256);
+        cfg.blockDim = dim3(GEMM_THREADS);
         cfg.dynamicSmemBytes = C::SMEM;
         cfg.stream = s;
         cudaLaunchAttribute attr[1];
