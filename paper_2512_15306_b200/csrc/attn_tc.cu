@@ -344,6 +344,286 @@ __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ C
 }
 
 
+
+// ===========================================================================
+// One-pass forward (online softmax).  Same roles and buffers as fwd_tc_kernel,
+// but every KV tile is visited once: S(j) = QK^T in TMEM (double-buffered);
+// the two softmax threads of a row (key halves) agree on the tile max through
+// shared memory; p~ = exp(x - m_used) with a lazily updated m_used (moved only
+// when the row max grows by more than 2^8, so p~ <= 256 and O is rescaled in
+// TMEM rarely -- after PV(j-1) has landed); P~ as bf16 hi + lo in double-
+// buffered smem; O += P~_hi V + P~_lo V.  At the end O / l (l = sum of p~)
+// is the reference's sum_k (p_k) v_k up to f32 rounding order.
+// ===========================================================================
+__device__ __forceinline__ void tmem_ld32_raw(uint32_t taddr, uint32_t (&r)[32]) { tmem_ld32(taddr, r); }
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+        "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+        "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+
+template <int HD>
+__global__ void __launch_bounds__(NT, 1) fwd1_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H, int Hkv,
+                                                        float inv_sqrt_d, uint16_t* __restrict__ out, int64_t ldo,
+                                                        float* __restrict__ out32, float* __restrict__ lse,
+                                                        uint32_t* __restrict__ amax) {
+    using S = Smem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+    uint64_t* q_full = bar + 0;
+    uint64_t* k_full = bar + 1;    // [2]
+    uint64_t* k_empty = bar + 3;   // [2]
+    uint64_t* v_full = bar + 5;    // [2]
+    uint64_t* v_empty = bar + 7;   // [2]
+    uint64_t* s_full = bar + 9;    // [2]
+    uint64_t* s_empty = bar + 11;  // [2]
+    uint64_t* p_full = bar + 13;   // [2]
+    uint64_t* p_empty = bar + 15;  // [2]
+    uint64_t* o_full = bar + 17;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 18);
+
+    const int qt = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
+    const int kvh = h / (H / Hkv);
+    const int d = H * HD;
+    const int nj = qt + 1;  // causal KV tiles (BQ == BKV)
+    const int row0 = b * T + qt * BQ;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) tma_prefetch(&tm);
+    if (warp == 1 && lane == 0) {
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], NSW);
+            mbar_init(&p_full[i], NSW);
+            mbar_init(&p_empty[i], 1);
+        }
+        mbar_init(o_full, 1);
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t s_base = smem_u32(sm);
+
+    if (warp == 0 && lane == 0) {
+        // ===== TMA producer: Q once, then (K, V) per tile =====
+        mbar_arrive_expect_tx(q_full, S::Q);
+        for (int c = 0; c < HD / 64; ++c) tma_load_2d(&tm, q_full, sm + S::OFF_Q + c * BQ * 128, h * HD + c * 64, row0);
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        for (int j = 0; j < nj; ++j) {
+            const int krow = b * T + j * BKV;
+            mbar_wait(&k_empty[ks], kph ^ 1);
+            mbar_arrive_expect_tx(&k_full[ks], S::K);
+            for (int c = 0; c < HD / 64; ++c)
+                tma_load_2d(&tm, &k_full[ks], sm + S::OFF_K + ks * S::K + c * BKV * 128, d + kvh * HD + c * 64, krow);
+            if (++ks == 2) { ks = 0; kph ^= 1; }
+            mbar_wait(&v_empty[vs], vph ^ 1);
+            mbar_arrive_expect_tx(&v_full[vs], S::V);
+            for (int c = 0; c < HD / 64; ++c)
+                tma_load_2d(&tm, &v_full[vs], sm + S::OFF_V + vs * S::V + c * BKV * 128, d + Hkv * HD + kvh * HD + c * 64,
+                            krow);
+            if (++vs == S::NVS) { vs = 0; vph ^= 1; }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: S(0), then S(j+1) ahead of PV(j) =====
+        const uint32_t idesc_s = make_idesc(1, 1, false, false, BQ, BKV);
+        const uint32_t idesc_o = make_idesc(1, 1, false, true, BQ, HD);
+        mbar_wait(q_full, 0);
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        auto issue_s = [&](int j) {
+            mbar_wait(&k_full[ks], kph);
+            const int sb = j & 1;
+            mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t qa = s_base + S::OFF_Q, ka = s_base + S::OFF_K + ks * S::K;
+#pragma unroll
+            for (int kk = 0; kk < HD / 16; ++kk)
+                mma_bf16_ss(tmem + sb * BKV, kdesc(qa, kk, BQ * 128), kdesc(ka, kk, BKV * 128), idesc_s, kk > 0);
+            tc_commit(&k_empty[ks]);
+            tc_commit(&s_full[sb]);
+            if (++ks == 2) { ks = 0; kph ^= 1; }
+        };
+        issue_s(0);
+        for (int j = 0; j < nj; ++j) {
+            if (j + 1 < nj) issue_s(j + 1);
+            const int pb = S::NPB == 2 ? (j & 1) : 0;
+            const uint32_t pph = S::NPB == 2 ? ((j >> 1) & 1) : (j & 1);
+            mbar_wait(&p_full[pb], pph);
+            mbar_wait(&v_full[vs], vph);
+            tc_fence_after();
+            const uint32_t va = s_base + S::OFF_V + vs * S::V;
+            const uint32_t ph = s_base + S::OFF_PH + pb * 2 * S::P, pl = ph + S::P;
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk) {
+                const uint64_t bd = mndesc(va, kk, BKV * 128);
+                mma_bf16_ss(tmem + 256, kdesc(ph, kk, BQ * 128), bd, idesc_o, (j | kk) != 0);
+                mma_bf16_ss(tmem + 256, kdesc(pl, kk, BQ * 128), bd, idesc_o, 1);
+            }
+            tc_commit(&v_empty[vs]);
+            tc_commit(&p_empty[pb]);
+            if (++vs == S::NVS) { vs = 0; vph ^= 1; }
+        }
+        tc_commit(o_full);
+    } else if (warp >= 4) {
+        // ===== softmax: thread = (query row, key half) =====
+        const int wq = warp & 3, half = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;
+        const int q = qt * BQ + r;
+        const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
+        const uint32_t o_cols = lane_base + 256 + half * (HD / 2);  // this thread's half of the O row
+        const int c0 = half * (BKV / 2);
+        const float a = inv_sqrt_d * LOG2E;
+        constexpr float RESCALE = 8.0f;  // log2 headroom of p~ before O is rescaled
+        float* xch = reinterpret_cast<float*>(sm + S::OFF_BAR + 256);  // [2][BQ] tile maxima, later l
+        const int pair_bar = 2 + wq;  // named barrier of the two warps sharing these rows
+        float m = -INFINITY, l = 0.0f;  // m: m_used in raw-score units; l: this half's sum of p~
+        for (int j = 0; j < nj; ++j) {
+            const int sb = j & 1;
+            mbar_wait(&s_full[sb], (j >> 1) & 1);
+            tc_fence_after();
+            uint32_t rr[64];
+            tmem_ld32(lane_base + sb * BKV + c0, *reinterpret_cast<uint32_t(*)[32]>(&rr[0]));
+            tmem_ld32(lane_base + sb * BKV + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&rr[32]));
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s_empty[sb]);
+            const bool diag = j == qt;
+            const int kbase = j * BKV + c0;
+            float mt = -INFINITY;
+            if (diag) {
+#pragma unroll
+                for (int i = 0; i < 64; ++i)
+                    if (kbase + i <= q) mt = fmaxf(mt, __uint_as_float(rr[i]));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 64; ++i) mt = fmaxf(mt, __uint_as_float(rr[i]));
+            }
+            xch[half * BQ + r] = mt;
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            mt = fmaxf(mt, xch[(half ^ 1) * BQ + r]);
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // xch reusable next tile
+            const int pb = S::NPB == 2 ? (j & 1) : 0;
+            const uint32_t pph = S::NPB == 2 ? ((j >> 1) & 1) : (j & 1);
+            // P buffer pb free (PV(j - NPB) done)
+            mbar_wait(&p_empty[pb], pph ^ 1);
+            const bool grow = mt > m && (m == -INFINITY || (mt - m) * a > RESCALE);
+            if (__any_sync(0xffffffffu, grow && m != -INFINITY)) {
+                // O holds PV(0..j-1): wait for PV(j-1), then scale this thread's O columns
+                if (j >= 1) {
+                    const int pb1 = S::NPB == 2 ? ((j - 1) & 1) : 0;
+                    const uint32_t ph1 = S::NPB == 2 ? (((j - 1) >> 1) & 1) : ((j - 1) & 1);
+                    mbar_wait(&p_empty[pb1], ph1);
+                }
+                tc_fence_after();
+                const float alpha = (grow && m != -INFINITY) ? ex2((m - mt) * a) : 1.0f;
+#pragma unroll
+                for (int c = 0; c < HD / 64; ++c) {
+                    uint32_t ov[32];
+                    tmem_ld32(o_cols + c * 32, ov);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                    tmem_st32(o_cols + c * 32, ov);
+                }
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                l *= alpha;
+            }
+            if (grow) m = mt;
+            const float mb = m * a;
+            uint8_t* ph = sm + S::OFF_PH + pb * 2 * S::P + half * BQ * 128;
+            uint8_t* pl = ph + S::P;
+            uint32_t hi[32], lo[32];
+            float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+            for (int i = 0; i < 64; i += 2) {
+                float pp[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const bool live = !diag || (kbase + i + e <= q);
+                    pp[e] = live ? ex2(__fmaf_rn(__uint_as_float(rr[i + e]), a, -mb)) : 0.0f;
+                }
+                s4[(i >> 1) & 3] += pp[0] + pp[1];
+                const float h0 = bf16r(pp[0]), h1 = bf16r(pp[1]);
+                hi[i / 2] = pack_bf16x2(h0, h1);
+                lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
+            }
+            l += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+                const int off = r * 128 + ((cc ^ (r & 7)) << 4);
+                *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[cc * 4 + 0], hi[cc * 4 + 1], hi[cc * 4 + 2], hi[cc * 4 + 3]);
+                *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[cc * 4 + 0], lo[cc * 4 + 1], lo[cc * 4 + 2], lo[cc * 4 + 3]);
+            }
+            fence_async_shared();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&p_full[pb]);
+        }
+        // l of the whole row
+        xch[half * BQ + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        const float lt = l + xch[(half ^ 1) * BQ + r];
+        const float inv_l = lt > 0.0f ? 1.0f / lt : 0.0f;
+        mbar_wait(o_full, 0);
+        tc_fence_after();
+        uint32_t mx = 0;
+        const bool valid = q < T;
+        const int64_t grow_ = (int64_t)b * T + q;
+#pragma unroll
+        for (int c = 0; c < HD / 64; ++c) {
+            const int col = half * (HD / 2) + c * 32;
+            uint32_t rr[32];
+            tmem_ld32(lane_base + 256 + col, rr);
+            tmem_ld_wait();
+            if (valid) {
+                uint4* o16 = reinterpret_cast<uint4*>(out + grow_ * ldo + h * HD + col);
+                float4* o32 = reinterpret_cast<float4*>(out32 + grow_ * ldo + h * HD + col);
+#pragma unroll
+                for (int v4 = 0; v4 < 4; ++v4) {
+                    float f[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        f[e] = __uint_as_float(rr[v4 * 8 + e]) * inv_l;
+                        mx = max(mx, abs_bits(bf16r(f[e])));
+                    }
+                    o16[v4] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                         pack_bf16x2(f[6], f[7]));
+                    if (out32) {
+                        o32[2 * v4] = make_float4(f[0], f[1], f[2], f[3]);
+                        o32[2 * v4 + 1] = make_float4(f[4], f[5], f[6], f[7]);
+                    }
+                }
+            }
+        }
+        if (valid && half == 0) lse[((int64_t)b * H + h) * T + q] = m * inv_sqrt_d + logf(lt);
+        mx = warp_max_u32(mx);
+        if (lane == 0 && amax && mx) atomicMax(amax, mx);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ===========================================================================
 // Backward on tcgen05 (reference sdpa_chunked_backward, src/tensorops.cpp:257-303).
 //
@@ -887,15 +1167,23 @@ extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, in
     if (rc) return rc;
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     dim3 grid((unsigned)ceil_div(T, BQ), H, B);
-    if (hd == 64) {
-        const int smem = Smem<64>::BYTES;
-        cudaFuncSetAttribute(fwd_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        fwd_tc_kernel<64><<<grid, NT, smem, s>>>(tm, T, H, Hkv, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, amax);
-    } else {
-        const int smem = Smem<128>::BYTES;
-        cudaFuncSetAttribute(fwd_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        fwd_tc_kernel<128><<<grid, NT, smem, s>>>(tm, T, H, Hkv, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, amax);
+    static int two_pass = -1;
+    if (two_pass < 0) {
+        const char* e = getenv("QTB_ATTN_FWD2");
+        two_pass = e ? atoi(e) : 0;  // 1: the two-pass (normalise-first) kernel
     }
+#define QTB_FWD(KERNEL, HDV)                                                                                      \
+    {                                                                                                            \
+        const int smem = Smem<HDV>::BYTES;                                                                       \
+        cudaFuncSetAttribute(KERNEL<HDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                    \
+        KERNEL<HDV><<<grid, NT, smem, s>>>(tm, T, H, Hkv, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, amax);   \
+    }
+    if (hd == 64) {
+        if (two_pass) QTB_FWD(fwd_tc_kernel, 64) else QTB_FWD(fwd1_tc_kernel, 64)
+    } else {
+        if (two_pass) QTB_FWD(fwd_tc_kernel, 128) else QTB_FWD(fwd1_tc_kernel, 128)
+    }
+#undef QTB_FWD
     return (int)cudaGetLastError();
 }
 
