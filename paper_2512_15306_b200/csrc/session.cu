@@ -102,11 +102,18 @@ __global__ void finalize_scale_kernel(const double* ssq, float mean_scale, float
     *norm_out = norm;
 }
 __global__ void set_scale_kernel(float* p, float v) { *p = v; }
+// E4M3 scales of n tensors from their absmax bit patterns (absmax_scale, src/numerics.cpp:150-158)
+__global__ void weight_scale_kernel(const uint32_t* __restrict__ amax, float* __restrict__ scale, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) scale[i] = absmax_scale(__uint_as_float(amax[i]), kE4M3);
+}
 // cross-worker sum in ascending worker order, plain f32 (src/trainer.cpp:95-102)
-__global__ void ordered_sum_kernel(const uint16_t* __restrict__ recv, int W, int64_t n, float* __restrict__ out) {
+// recv holds W rank blocks of `stride` elements; sums elements [0, n) of each
+__global__ void ordered_sum_kernel(const uint16_t* __restrict__ recv, int W, int64_t n, int64_t stride,
+                                   float* __restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float s = bfbits2f(recv[i]);
-        for (int w = 1; w < W; ++w) s = __fadd_rn(s, bfbits2f(recv[(int64_t)w * n + i]));
+        for (int w = 1; w < W; ++w) s = __fadd_rn(s, bfbits2f(recv[(int64_t)w * stride + i]));
         out[i] = s;
     }
 }
@@ -157,6 +164,11 @@ class Session {
     uint64_t seed;
     int rank, world;
     cudaStream_t st = nullptr;
+    cudaStream_t cst = nullptr;  // communication stream (per-layer gradient exchange, shard_grads)
+    cudaEvent_t ev_grad = nullptr, ev_comm = nullptr;
+    std::vector<int64_t> soff_of;  // offset of each tensor's shard in the W x shard_total exchange layout
+    bool comm_pending = false;
+    bool exchange_in_backward = false;  // shard_grads: per-layer exchange during this backward
     ncclComm_t comm = nullptr;
 
     int L, d, F, Hh, H, Hkv, hd, q, T;
@@ -263,6 +275,9 @@ class Session {
             std::memcpy(&id, nccl_id, sizeof(id));
             ncclResult_t r = api.CommInitRank(&comm, world, id, rank);
             if (r != ncclSuccess) throw QtError(3, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+            QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+            QT_CHECK_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
+            QT_CHECK_CUDA(cudaEventCreateWithFlags(&ev_comm, cudaEventDisableTiming));
         }
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
@@ -270,6 +285,9 @@ class Session {
     ~Session() {
         if (comm) NcclApi::get().CommDestroy(comm);
         for (auto e : ev_pool) cudaEventDestroy(e);
+        if (ev_grad) cudaEventDestroy(ev_grad);
+        if (ev_comm) cudaEventDestroy(ev_comm);
+        if (cst) cudaStreamDestroy(cst);
         if (arena) cudaFree(arena);
         if (st) cudaStreamDestroy(st);
     }
@@ -323,7 +341,11 @@ class Session {
         add_param("final_g", {d});
         add_param("lm_head", {V, d});
         shard_total = 0;
-        for (auto& t : P) shard_total += t.pw;
+        soff_of.clear();
+        for (auto& t : P) {
+            soff_of.push_back(shard_total);
+            shard_total += t.pw;
+        }
     }
     const ParamT& par(const std::string& n) const { return P.at(pidx.at(n)); }
     uint16_t* pptr(const std::string& n) { return params + par(n).off; }
@@ -369,11 +391,11 @@ class Session {
             req(&recvbuf, (size_t)world * shard_total * 2);
         }
         wcodes.assign((size_t)L * 4, nullptr);
-        for (int l = 0; l < L; ++l) {
-            req(&wcodes[l * 4 + W_QKV], (size_t)q * d);
-            req(&wcodes[l * 4 + W_O], (size_t)d * d);
-            req(&wcodes[l * 4 + W_GU], (size_t)F * d);
-            req(&wcodes[l * 4 + W_DOWN], (size_t)d * Hh);
+        for (int l = 0; l < L; ++l) {  // padded to W*pw: shard_weights all-gathers the codes in place
+            req(&wcodes[l * 4 + W_QKV], (size_t)P[lp(l, 1)].padded);
+            req(&wcodes[l * 4 + W_O], (size_t)P[lp(l, 2)].padded);
+            req(&wcodes[l * 4 + W_GU], (size_t)P[lp(l, 4)].padded);
+            req(&wcodes[l * 4 + W_DOWN], (size_t)P[lp(l, 5)].padded);
         }
         lb.assign(L + 1, LayerBufs());
         // shared scratch for dropped sites
@@ -629,8 +651,56 @@ class Session {
     int gkind() const { return prec.backward_grads == 0 ? kE4M3 : kE5M2; }
 
     // ---------------- StepContext (src/model.cpp:88-107) ----------------
+    bool shard_weights() const { return plan.shard_weights && world > 1; }
+    bool shard_grads() const { return plan.shard_grads && world > 1; }
+    // w_qkv, w_o, w_gate_up, w_down of some layer (for_each_param order, model.hpp:107-121)
+    bool is_block_weight(int pi) const {
+        if (pi < 1 || pi > 6 * L) return false;
+        const int k = (pi - 1) % 6;
+        return k == 1 || k == 2 || k == 4 || k == 5;
+    }
+
     void build_step_context() {
         QT_CHECK_CUDA(cudaMemsetAsync(w_amax, 0, L * 16, st));
+        if (shard_weights()) {
+            // RunPlan::shard_weights: each rank holds only its ZeRO-1 slice of the block
+            // weights.  Per-tensor absmax = max over the ranks' slice maxima (all-reduce MAX of
+            // the u32 |x| bit patterns), each rank casts its slice with that scale, and the
+            // E4M3 codes (1 B/param, half the bf16 traffic) are all-gathered in place.
+            // Codes equal a cast of the full tensor bit for bit (the cast is elementwise).
+            auto& api = NcclApi::get();
+            for (int l = 0; l < L; ++l) {
+                const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
+                for (int k = 0; k < 4; ++k) {
+                    const ParamT& t = P[widx[k]];
+                    const int64_t lo = std::min<int64_t>((int64_t)rank * t.pw, t.numel);
+                    const int64_t n = std::min<int64_t>(t.pw, t.numel - lo);
+                    if (n > 0) QT_CHECK_K(qtk_absmax_bf16(params + t.off + lo, n, w_amax + l * 4 + k, st));
+                }
+            }
+            ncclResult_t r = api.AllReduce(w_amax, w_amax, (size_t)L * 4, ncclUint32, ncclMax, comm, st);
+            if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight absmax: ") + api.GetErrorString(r));
+            weight_scale_kernel<<<(unsigned)ceil_div(L * 4, 128), 128, 0, st>>>(w_amax, w_scale, L * 4);  // ranks with an empty slice
+            QT_CHECK_CUDA(cudaGetLastError());
+            api.GroupStart();
+            for (int l = 0; l < L; ++l) {
+                const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
+                for (int k = 0; k < 4; ++k) {
+                    const ParamT& t = P[widx[k]];
+                    const int64_t lo = (int64_t)rank * t.pw;
+                    const int64_t n = std::max<int64_t>(0, std::min<int64_t>(t.pw, t.numel - lo));
+                    const int h = prof_begin();
+                    if (n > 0)
+                        QT_CHECK_K(qtk_quantize_bf16(params + t.off + lo, n, kE4M3, w_amax + l * 4 + k,
+                                                     wcodes[l * 4 + k] + lo, w_scale + l * 4 + k, st));
+                    prof_end(h, 3, 3.0 * n);
+                    api.AllGather(wcodes[l * 4 + k] + lo, wcodes[l * 4 + k], (size_t)t.pw, ncclUint8, comm, st);
+                }
+            }
+            r = api.GroupEnd();
+            if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight-code all-gather: ") + api.GetErrorString(r));
+            return;
+        }
         for (int l = 0; l < L; ++l) {
             const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
             for (int k = 0; k < 4; ++k) {
@@ -818,6 +888,7 @@ class Session {
                                        dgamma, l > 0 ? g_amax + (l - 1) * 4 + G_DR : nullptr, st));
             accumulate_f32(P[lp(l, 0)], dgamma, micro_step);
             prof_end(h, 4, 10.0 * M * d);
+            if (exchange_in_backward) reduce_layer_async(l);
         }
         // ordered embedding backward, bf16 round, accumulate (model.cpp:442-444)
         {
@@ -835,31 +906,54 @@ class Session {
     }
 
     // ---------------- cross-rank gradient reduction (ZeRO-1) ----------------
-    // all-to-all of bf16 shards + ascending-rank f32 sum == trainer.cpp:90-103 bitwise
-    void reduce_grads() {
+    // all-to-all of bf16 shards + ascending-rank f32 sum == trainer.cpp:90-103 bitwise,
+    // for the tensors [i0, i1) of the parameter list, on stream s
+    void reduce_tensors(int i0, int i1, cudaStream_t s) {
         auto& api = NcclApi::get();
-        const int h = prof_begin();
         api.GroupStart();
-        int64_t soff = 0;
-        for (auto& t : P) {
+        for (int i = i0; i < i1; ++i) {
+            const ParamT& t = P[i];
+            const int64_t soff = soff_of[i];
             for (int j = 0; j < world; ++j) {
-                uint16_t* dst = recvbuf + (int64_t)j * shard_total + soff;
                 const uint16_t* src = grads + t.off + (int64_t)j * t.pw;
                 if (j == rank) {
                     cudaMemcpyAsync(recvbuf + (int64_t)rank * shard_total + soff, src, t.pw * 2,
-                                    cudaMemcpyDeviceToDevice, st);
+                                    cudaMemcpyDeviceToDevice, s);
                 } else {
-                    api.Send(src, (size_t)t.pw, ncclBfloat16, j, comm, st);
-                    api.Recv(dst, (size_t)t.pw, ncclBfloat16, j, comm, st);
+                    api.Send(src, (size_t)t.pw, ncclBfloat16, j, comm, s);
+                    api.Recv(recvbuf + (int64_t)j * shard_total + soff, (size_t)t.pw, ncclBfloat16, j, comm, s);
                 }
             }
-            soff += t.pw;
         }
         ncclResult_t r = api.GroupEnd();
         if (r != ncclSuccess) throw QtError(3, std::string("NCCL grad exchange: ") + api.GetErrorString(r));
-        ordered_sum_kernel<<<grid_for(shard_total), 256, 0, st>>>(recvbuf, world, shard_total, gshard);
+        const int64_t n = soff_of[i1 - 1] + P[i1 - 1].pw - soff_of[i0];
+        ordered_sum_kernel<<<grid_for(n), 256, 0, s>>>(recvbuf + soff_of[i0], world, n, shard_total,
+                                                      gshard + soff_of[i0]);
         QT_CHECK_CUDA(cudaGetLastError());
+    }
+    void reduce_grads() {
+        const int h = prof_begin();
+        reduce_tensors(0, (int)P.size(), st);
         prof_end(h, 9, 2.0 * shard_total * (world - 1) * 2);
+    }
+    // RunPlan::shard_grads: layer l's gradients are final once its backward is done (last
+    // micro-batch): exchange them on the communication stream while layers l-1..0 run
+    void reduce_layer_async(int l) {
+        QT_CHECK_CUDA(cudaEventRecord(ev_grad, st));
+        QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_grad, 0));
+        reduce_tensors(lp(l, 0), lp(l, 5) + 1, cst);
+        comm_pending = true;
+    }
+    void reduce_rest_and_join() {
+        // embed (index 0) and final_g / lm_head (the last two) on the comm stream, then join
+        QT_CHECK_CUDA(cudaEventRecord(ev_grad, st));
+        QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_grad, 0));
+        reduce_tensors(0, 1, cst);
+        reduce_tensors((int)P.size() - 2, (int)P.size(), cst);
+        QT_CHECK_CUDA(cudaEventRecord(ev_comm, cst));
+        QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_comm, 0));
+        comm_pending = false;
     }
 
     void grad_sumsq() {
@@ -888,9 +982,12 @@ class Session {
             auto& api = NcclApi::get();
             h = prof_begin();
             api.GroupStart();
-            for (auto& t : P)
+            for (int i = 0; i < (int)P.size(); ++i) {
+                if (shard_weights() && is_block_weight(i)) continue;  // gathered as FP8 codes next step
+                const ParamT& t = P[i];
                 api.AllGather(params + t.off + (int64_t)rank * t.pw, params + t.off, (size_t)t.pw, ncclBfloat16, comm,
                               st);
+            }
             ncclResult_t r = api.GroupEnd();
             if (r != ncclSuccess) throw QtError(3, std::string("NCCL param all-gather: ") + api.GetErrorString(r));
             prof_end(h, 9, 2.0 * shard_total * (world - 1));
@@ -906,9 +1003,16 @@ class Session {
         for (int ga = 0; ga < GA; ++ga) {
             forward(tokens + (int64_t)ga * tokens_per_mb, tokens_per_mb, batch, true);
             QT_CHECK_CUDA(cudaMemcpyAsync(loss_dev + 1 + ga, loss_dev, 4, cudaMemcpyDeviceToDevice, st));
+            // shard_grads: the final gradients of layer l are exchanged while layers < l run
+            // backward (last micro-batch only, so the summation order stays trainer.cpp:90-103)
+            exchange_in_backward = shard_grads() && ga == GA - 1;
             backward((uint64_t)step * GA + ga);
+            exchange_in_backward = false;
         }
-        if (world > 1) reduce_grads();
+        if (world > 1) {
+            if (shard_grads()) reduce_rest_and_join();
+            else reduce_grads();
+        }
         grad_sumsq();
         const float mean_scale = 1.0f / (static_cast<float>(GA) * world);
         finalize_scale_kernel<<<1, 1, 0, st>>>(ssq_dev, mean_scale, max_norm, gscale_dev, norm_dev);

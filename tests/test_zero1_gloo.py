@@ -103,3 +103,66 @@ def test_zero1_step_world2_matches_single_process():
         assert abs(norm - np.sqrt(ssq)) / np.sqrt(ssq) < 1e-12
         for n in SIZES:
             np.testing.assert_array_equal(np.frombuffer(newp[n], np.float32), want[n], err_msg=f"rank {rank} {n}")
+
+
+# ---------------------------------------------------------------------------
+# RunPlan::shard_weights: every rank holds only its ZeRO-1 slice of a block
+# weight; the per-tensor absmax is the all-reduce MAX of the slice maxima, each
+# rank casts its slice with that scale and the E4M3 codes are all-gathered
+# (session.cu build_step_context).  Must equal the full-tensor cast bitwise.
+# ---------------------------------------------------------------------------
+WSIZES = {"layers.0.w_qkv": 3000, "layers.0.w_o": 1024, "layers.1.w_down": 777}
+
+
+def _weights():
+    return {n: bf16_grid_round(rng_floats(900 + i, s, -2, 2) * (1 + i)) for i, (n, s) in enumerate(WSIZES.items())}
+
+
+def _worker_codes(rank, world, port_num, out_q):
+    import torch.distributed as dist
+    from oracle import port
+    from paper_2512_15306_b200 import session as S
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_num)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = {}
+    for n, w in _weights().items():
+        padded, pw = S.shard_layout(w.size, world)
+        lo, hi = min(rank * pw, w.size), min((rank + 1) * pw, w.size)
+        local = port.absmax(w[lo:hi]) if lo < hi else 0.0
+        t = torch.tensor([np.float32(local).view(np.int32)], dtype=torch.int32)  # |x| bit patterns order like floats
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        amax = float(np.int32(t.item()).view(np.float32))
+        codes = np.zeros(pw, np.uint8)
+        if lo < hi:
+            codes[:hi - lo] = port.quantize_with_absmax(w[lo:hi], 0, amax)[0]
+        parts = [torch.zeros(pw, dtype=torch.uint8) for _ in range(world)]
+        dist.all_gather(parts, torch.from_numpy(codes))
+        out[n] = (torch.cat(parts).numpy()[:w.size].tobytes(), port.absmax_scale(amax, 0))
+    out_q.put((rank, out))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_shard_weights_code_allgather_matches_full_cast(world):
+    import socket
+    import torch.multiprocessing as mp
+    from oracle import port
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port_num = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_codes, args=(r, world, port_num, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    for n, w in _weights().items():
+        amax = port.absmax(w)
+        want_codes, want_scale = port.quantize_with_absmax(w, 0, amax)
+        for rank, out in res:
+            got, scale = out[n]
+            np.testing.assert_array_equal(np.frombuffer(got, np.uint8), want_codes, err_msg=f"rank {rank} {n}")
+            assert scale == want_scale
