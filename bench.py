@@ -103,37 +103,38 @@ def _ref_worker(args):
     return _ref_sample_seconds(cfg7, layers, tps, seed)
 
 
-def cpu_reference_rate(cfg, sample_tokens: int, cores: int, reps: int = 1) -> dict:
-    """tokens/s of the reference step (src/trainer.cpp:64-110) for the full
-    model, extrapolated from one- and two-layer samples at the real widths and
-    vocabulary ('measured as samples ... labelled extrapolated')."""
-    import multiprocessing as mp
+def cpu_reference_model(cfg, sample_tokens: int) -> dict:
+    """Per-token cost model of the reference step (src/trainer.cpp:64-110) for the
+    full model from one- and two-layer samples at the real widths and vocabulary
+    ('measured as samples ... labelled extrapolated')."""
     cfg7 = cfg.as_list()
     t1 = _ref_sample_seconds(cfg7, 1, sample_tokens, 1)
     t2 = _ref_sample_seconds(cfg7, 2, sample_tokens, 2)
     per_layer = max(t2 - t1, 1e-9)
     base = max(t1 - per_layer, 0.0)
     t_full = base + cfg.n_layers * per_layer  # seconds per sample_tokens tokens, one core
-    rate1 = sample_tokens / t_full
-    wall = 0.0
+    return {"t1": t1, "t2": t2, "t_full": t_full, "rate_1core": sample_tokens / t_full}
+
+
+def cpu_reference_rate(cfg, sample_tokens: int, cores: int, model: dict | None = None) -> dict:
+    """tokens/s of the reference step on `cores` host cores: the one-core rate of
+    the cost model, times the measured parallel efficiency of `cores`
+    independent reference processes each running the one-layer sample."""
+    import multiprocessing as mp
+    m = model or cpu_reference_model(cfg, sample_tokens)
+    rate, wall = m["rate_1core"], 0.0
     if cores > 1:
-        # all host cores: independent reference processes on distinct samples
+        cfg7 = cfg.as_list()
         t0 = time.perf_counter()
         with mp.get_context("spawn").Pool(cores) as pool:
-            ts = pool.map(_ref_worker, [(cfg7, 1, sample_tokens, 10 + i) for i in range(cores * reps)])
+            ts = pool.map(_ref_worker, [(cfg7, 1, sample_tokens, 10 + i) for i in range(cores)])
         wall = time.perf_counter() - t0
-        # aggregate = cores x single-core rate scaled by the measured parallel efficiency
-        eff = (sum(ts) / len(ts)) * reps / wall * cores / cores if wall > 0 else 1.0
-        rate = rate1 * cores * min(1.0, (sum(ts) / max(wall, 1e-9)) / cores)
-        del eff
-    else:
-        rate = rate1
-    return {"value": rate, "rate_1core": rate1, "t_sample_1layer_s": t1, "t_sample_2layer_s": t2,
+        rate = m["rate_1core"] * cores * min(1.0, (sum(ts) / max(wall, 1e-9)) / cores)
+    return {"value": rate, "rate_1core": m["rate_1core"], "t_sample_1layer_s": m["t1"], "t_sample_2layer_s": m["t2"],
             "sample_tokens": sample_tokens, "wall_s": wall}
 
 
 def run_reference_arm(args, cfg, B, T, world):
-    import multiprocessing as mp
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -143,11 +144,8 @@ def run_reference_arm(args, cfg, B, T, world):
         return
     cores = os.cpu_count() or 1
     sample_tokens = args.ref_sample_tokens
-    times = []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_rate(cfg, sample_tokens, cores if i >= args.warmup else 1)
-        if i >= args.warmup:
-            times.append(r["value"])
+    model = cpu_reference_model(cfg, sample_tokens)  # warm-up + the per-layer cost model
+    times = [cpu_reference_rate(cfg, sample_tokens, cores, model)["value"] for _ in range(args.steps)]
     value = statistics.median(times)
     fp8_f, bf16_f = cfg.flops_per_token()
     line = {
@@ -158,9 +156,10 @@ def run_reference_arm(args, cfg, B, T, world):
                    "parallelism": "cpu processes"},
         "mfu": value * (fp8_f / P_FP8_SPEC + bf16_f / P_BF16_SPEC),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference",
-                         "sample": f"reference train step (src/trainer.cpp:64-110) on 1- and 2-layer samples at the "
-                                   f"real widths/vocab with {sample_tokens} tokens, extrapolated to {cfg.n_layers} "
-                                   f"layers; {cores} independent processes"},
+                         "sample": f"unmodified reference train step (src/trainer.cpp:64-110, oracle/_ref) on 1- and "
+                                   f"2-layer samples at the real widths/vocab with {sample_tokens} tokens, extrapolated "
+                                   f"to {cfg.n_layers} layers (t1={model['t1']:.2f}s t2={model['t2']:.2f}s); each "
+                                   f"step = {cores} independent reference processes"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
