@@ -59,7 +59,10 @@ enum {
     EPI_F32 = 1,      /* out f32 = acc                                                   */
     EPI_BF16_RES = 2, /* out bf16 = bf16(bf16(acc/(sa*sb)) + res)                        */
     EPI_BF16_ACC = 3, /* out (bf16 grad buffer) = SR(out + bf16(acc/(sa*sb)))            */
-    EPI_F32_ACC = 4   /* out (bf16 grad buffer) = SR(out + acc)                          */
+    EPI_F32_ACC = 4,  /* out (bf16 grad buffer) = SR(out + acc)                          */
+    EPI_SWIGLU_BWD = 5 /* acc = dh (bf16(acc/(sa*sb))); res = gate|up (M x 2N bf16);      */
+                       /* out (M x 2N) = swiglu_backward(gate|up, dh) (tensorops.cpp:133-153) */
+                       /* + absmax of out into amax                                        */
 };
 
 typedef struct QtkGemm {
@@ -85,6 +88,7 @@ typedef struct QtkGemm {
     void* ws;           /* optional split-K workspace (f32); NULL = no split               */
     int64_t ws_bytes;
     int split_k;        /* 0 = auto (only when the tile grid starves the SMs), 1 = off     */
+    uint32_t* amax;     /* EPI_SWIGLU_BWD: absmax (u32 |x| bits) of the output              */
 } QtkGemm;
 
 int qtk_gemm(const QtkGemm* g, cudaStream_t s);

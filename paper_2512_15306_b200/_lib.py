@@ -23,7 +23,7 @@ class QtkGemm(C.Structure):
         ("a_scale", c_vp), ("b_scale", c_vp),
         ("epi", C.c_int), ("out", c_vp), ("ldo", c_i64), ("res", c_vp), ("ldr", c_i64),
         ("sr_seed", c_u64), ("sr_stream", c_u64), ("sr_base", c_u64), ("bn", C.c_int), ("a2", c_vp),
-        ("ws", c_vp), ("ws_bytes", c_i64), ("split_k", C.c_int),
+        ("ws", c_vp), ("ws_bytes", c_i64), ("split_k", C.c_int), ("amax", c_vp),
     ]
 
 

@@ -42,6 +42,7 @@ struct alignas(64) Params {
     CUtensorMap to;   // output (and EPI_*_ACC accumulator) map, 128-B x 32-row boxes
     CUtensorMap tr;   // EPI_BF16_RES residual map
     int tma_out;      // epilogue stages tiles through smem and stores them with TMA
+    uint32_t* amax;   // EPI_SWIGLU_BWD: absmax of the output
     int n_fast;       // tile order: N-tiles of one M panel adjacent (they share the A panel in L2)
     int M, N, K;
     int num_m, num_n, num_k;
@@ -59,7 +60,9 @@ struct alignas(64) Params {
 
 // CG = CTAs per MMA (tcgen05 cta_group): 2 pairs two SMs on a 256-row tile
 // and splits the B tile between them (half the per-SM operand traffic)
-__host__ __device__ constexpr bool epi_loads(int epi) { return epi == EPI_BF16_RES || epi == EPI_BF16_ACC || epi == EPI_F32_ACC; }
+__host__ __device__ constexpr bool epi_loads(int epi) {
+    return epi == EPI_BF16_RES || epi == EPI_BF16_ACC || epi == EPI_F32_ACC || epi == EPI_SWIGLU_BWD;
+}
 
 template <int KIND, int BN, int CG = 1, int EPI = EPI_BF16>
 struct Cfg {
@@ -76,7 +79,7 @@ struct Cfg {
     // 8 epilogue warps (two per TMEM lane quarter, each owning half of the
     // tile's columns); a LOADS warp keeps its whole 32 x BN/2 slice
     static constexpr int EPI_WARPS = 8;
-    static constexpr int EPI_GROUPS = epi_loads(EPI) ? BN / 128 : 1;
+    static constexpr int EPI_GROUPS = EPI == EPI_SWIGLU_BWD ? 2 : (epi_loads(EPI) ? BN / 128 : 1);
     static constexpr int EPI_BYTES = EPI_WARPS * EPI_GROUPS * 4096;
     static constexpr int STAGE_BUDGET = 232448 - 1536 - EPI_BYTES;  // 227 KB opt-in max, less align + barriers
     static constexpr int STAGES = STAGE_BUDGET / STAGE > 8 ? 8 : STAGE_BUDGET / STAGE;
@@ -190,6 +193,12 @@ template <int EPI>
 __device__ __forceinline__ void epilogue_prefetch(const Params& p, int m_row0, int n0, int BNt, uint8_t* stg,
                                                   uint64_t* ebar) {
     bulk_wait_read<0>();  // the previous tile's stores have left these boxes
+    if constexpr (EPI == EPI_SWIGLU_BWD) {  // group 0's gate and up boxes (later groups load in turn)
+        mbar_arrive_expect_tx(ebar, 2 * 4096);
+        tma_load_2d(&p.tr, ebar, stg, n0, m_row0);
+        tma_load_2d(&p.tr, ebar, stg + 4096, n0 + p.N, m_row0);
+        return;
+    }
     const int ng = max(0, min(BNt, p.N - n0 + 63)) / 64;  // 0 when this half lies past N
     mbar_arrive_expect_tx(ebar, ng * 4096);
     for (int g = 0; g < ng; ++g) tma_load_2d(EPI == EPI_BF16_RES ? &p.tr : &p.to, ebar, stg + g * 4096, n0 + g * 64, m_row0);
@@ -205,18 +214,30 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
     const int lane = threadIdx.x & 31;
     const int row = m_row0 + lane;
     const uint64_t key = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) ? rng_key(p.sr_seed, p.sr_stream) : 0;
-    if constexpr (LOADS) {
+    constexpr bool SWI = EPI == EPI_SWIGLU_BWD;
+    if constexpr (LOADS && !SWI) {
         mbar_wait(ebar, ephase);
         ephase ^= 1;
     }
+    uint32_t smax = 0;
     for (int g = 0; g < BNt / GC; ++g) {
         const int col0 = n0 + g * GC;
         if (col0 >= p.N) break;
+        if constexpr (SWI) {
+            if (g > 0 && lane == 0) {  // this group's gate / up boxes, once the previous stores have read them
+                bulk_wait_read<0>();
+                mbar_arrive_expect_tx(ebar, 2 * 4096);
+                tma_load_2d(&p.tr, ebar, stg, col0, m_row0);
+                tma_load_2d(&p.tr, ebar, stg + 4096, col0 + p.N, m_row0);
+            }
+        }
         uint32_t r[GC];
         tmem_ld32(tmem_cols + g * GC, *reinterpret_cast<uint32_t(*)[32]>(&r[0]));
         if constexpr (GC == 64) tmem_ld32(tmem_cols + g * GC + 32, *reinterpret_cast<uint32_t(*)[32]>(&r[32]));
         uint8_t* box;
-        if constexpr (LOADS) {
+        if constexpr (SWI) {
+            box = stg;
+        } else if constexpr (LOADS) {
             box = stg + g * 4096;
         } else {
             box = stg;
@@ -237,6 +258,43 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
             for (int j = 0; j < GC; ++j) v[j] = bf16r(div_exact(__uint_as_float(r[j]), denom, rcp));
         }
         uint4* rowp = reinterpret_cast<uint4*>(box + lane * 128);
+        if constexpr (SWI) {
+            // dh = bf16(acc / (sa*sb)) (the reference's dgrad output), then swiglu_backward
+            // (tensorops.cpp:133-153) with gate / up from the staged boxes, in place
+            mbar_wait(ebar, ephase);
+            ephase ^= 1;
+            uint4* rowu = reinterpret_cast<uint4*>(box + 4096 + lane * 128);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int sl = c ^ (lane & 7);
+                const uint4 ug = rowp[sl], uu = rowu[sl];
+                const uint32_t wg[4] = {ug.x, ug.y, ug.z, ug.w}, wu[4] = {uu.x, uu.y, uu.z, uu.w};
+                float dg[8], du[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float gv = e & 1 ? __uint_as_float(wg[e >> 1] & 0xFFFF0000u) : __uint_as_float(wg[e >> 1] << 16);
+                    const float uv = e & 1 ? __uint_as_float(wu[e >> 1] & 0xFFFF0000u) : __uint_as_float(wu[e >> 1] << 16);
+                    const float go = v[c * 8 + e];
+                    const float sig = __frcp_rn(__fadd_rn(1.0f, expf(-gv)));
+                    const float dsilu = __fmul_rn(sig, __fadd_rn(1.0f, __fmul_rn(gv, __fsub_rn(1.0f, sig))));
+                    dg[e] = bf16r(__fmul_rn(__fmul_rn(go, uv), dsilu));
+                    du[e] = bf16r(__fmul_rn(go, __fmul_rn(gv, sig)));
+                    smax = max(smax, max(abs_bits(dg[e]), abs_bits(du[e])));
+                }
+                rowp[sl] = make_uint4(pack_bf16x2(dg[0], dg[1]), pack_bf16x2(dg[2], dg[3]), pack_bf16x2(dg[4], dg[5]),
+                                      pack_bf16x2(dg[6], dg[7]));
+                rowu[sl] = make_uint4(pack_bf16x2(du[0], du[1]), pack_bf16x2(du[2], du[3]), pack_bf16x2(du[4], du[5]),
+                                      pack_bf16x2(du[6], du[7]));
+            }
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&p.to, box, col0, m_row0);
+                tma_store_2d(&p.to, box + 4096, col0 + p.N, m_row0);
+                bulk_commit();
+            }
+            continue;
+        }
         if constexpr (LOADS) {
             const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
 #pragma unroll
@@ -276,6 +334,10 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
             bulk_commit();
         }
         buf ^= 1;
+    }
+    if constexpr (SWI) {
+        smax = warp_max_u32(smax);
+        if (lane == 0 && smax) atomicMax(p.amax, smax);
     }
 }
 
@@ -664,6 +726,7 @@ int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, i
     QTB_GEMM_CASE(0, false, false, EPI_BF16)
     QTB_GEMM_CASE(0, false, false, EPI_BF16_RES)
     QTB_GEMM_CASE(0, false, true, EPI_BF16)
+    QTB_GEMM_CASE(0, false, true, EPI_SWIGLU_BWD)
     QTB_GEMM_CASE(0, true, true, EPI_BF16)
     QTB_GEMM_CASE(0, true, true, EPI_BF16_ACC)
     QTB_GEMM_CASE(0, true, true, EPI_F32)
@@ -809,7 +872,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     int splits = 1;
     // the reduce pass works on 4-column vectors with 32-bit indices
     const bool reducible = g->N % 4 == 0 && g->ldo % 4 == 0 && g->M * g->N / 4 < (int64_t(1) << 31);
-    if (g->ws && g->split_k != 1 && reducible) {
+    if (g->ws && g->split_k != 1 && reducible && g->epi != EPI_SWIGLU_BWD) {
         splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn, cg);
         if ((int64_t)splits * g->M * g->N * 4 > g->ws_bytes) splits = 1;
     }
@@ -842,13 +905,20 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
             const char* e = getenv("QTB_GEMM_NO_TMA_EPI");
             no_tma = e ? atoi(e) : 0;
         }
+        const int64_t ncols = g->epi == EPI_SWIGLU_BWD ? 2 * g->N : g->N;  // gate | up halves
         bool ok = !no_tma && !(reinterpret_cast<uintptr_t>(g->out) & 15) && ((g->ldo * oel) & 15) == 0 &&
-                  g->ldo >= g->N;
+                  g->ldo >= ncols;
         if (ok && g->epi == EPI_BF16_RES)
             ok = g->res && !(reinterpret_cast<uintptr_t>(g->res) & 15) && ((g->ldr * 2) & 15) == 0 && g->ldr >= g->N;
-        if (ok) ok = make_tmap(&p.to, g->out, oel, g->N, g->M, g->ldo, 128 / oel, 32) == 0;
-        if (ok && g->epi == EPI_BF16_RES) ok = make_tmap(&p.tr, g->res, 2, g->N, g->M, g->ldr, 64, 32) == 0;
+        if (ok && g->epi == EPI_SWIGLU_BWD)
+            ok = g->res && g->amax && !(reinterpret_cast<uintptr_t>(g->res) & 15) && ((g->ldr * 2) & 15) == 0 &&
+                 g->ldr >= ncols && g->N % 64 == 0;
+        if (ok) ok = make_tmap(&p.to, g->out, oel, ncols, g->M, g->ldo, 128 / oel, 32) == 0;
+        if (ok && (g->epi == EPI_BF16_RES || g->epi == EPI_SWIGLU_BWD))
+            ok = make_tmap(&p.tr, g->res, 2, ncols, g->M, g->ldr, 64, 32) == 0;
         p.tma_out = ok ? 1 : 0;
+        p.amax = g->amax;
+        if (g->epi == EPI_SWIGLU_BWD && !ok) return 1;  // no direct-store variant of this epilogue
     }
     const int grid = std::min(tiles, num_sms() / cg) * cg;
     return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, cg, s);

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -614,7 +615,7 @@ class Session {
     void gemm(int kind, int afmt, int bfmt, bool a_mn, bool b_mn, int64_t M, int64_t N, int64_t K, const void* a,
               int64_t lda, const void* b, int64_t ldb, const float* as, const float* bs, int epi, void* out,
               int64_t ldo, const void* res = nullptr, int64_t ldr = 0, uint64_t sr_seed = 0, uint64_t sr_stream = 0,
-              uint64_t sr_base = 0, const void* a2 = nullptr) {
+              uint64_t sr_base = 0, const void* a2 = nullptr, uint32_t* amax = nullptr) {
         QtkGemm g{};
         g.kind = kind;
         g.a_fmt = afmt;
@@ -643,12 +644,23 @@ class Session {
         g.ws = gemm_ws;
         g.ws_bytes = gemm_ws_bytes;
         g.split_k = 0;
+        g.amax = amax;
         const int h = prof_begin();
         QT_CHECK_K(qtk_gemm(&g, st));
         prof_end(h, kind == 0 ? 0 : 1, 2.0 * M * N * K * (a2 ? 2 : 1));
     }
 
     int gkind() const { return prec.backward_grads == 0 ? kE4M3 : kE5M2; }
+    bool fuse_swiglu_bwd() const {
+        static int f = -1;
+        if (f < 0) {
+            // off by default: the sigmoid/exp math concentrated in 8 epilogue warps per SM costs
+            // more than the d_h round trip it saves (measured +70 us/layer at 0.5B)
+            const char* e = getenv("QTB_FUSE_SWIGLU_BWD");
+            f = e ? atoi(e) : 0;
+        }
+        return f && Hh % 64 == 0;
+    }
 
     // ---------------- StepContext (src/model.cpp:88-107) ----------------
     bool shard_weights() const { return plan.shard_weights && world > 1; }
@@ -840,11 +852,18 @@ class Session {
             prof_end(h, 3, 3.0 * M * d);
             gemm(0, gk, kE4M3, true, true, d, Hh, M, gcodes, d, b.hc, Hh, gs + G_DR, as + S_H, EPI_BF16_ACC,
                  grads + pd.off, Hh, nullptr, 0, aseed, pd.s_acc, micro_step * (uint64_t)pd.numel);
-            gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wcodes[l * 4 + W_DOWN], Hh, gs + G_DR, ws + W_DOWN,
-                 EPI_BF16, d_h, Hh);
-            h = prof_begin();
-            QT_CHECK_K(qtk_swiglu_bwd(b.gu, d_h, M, Hh, d_gu, ga + G_DGU, st));
-            prof_end(h, 5, 2.0 * M * F * 2 + 2.0 * M * Hh);
+            if (fuse_swiglu_bwd()) {
+                // d_h = down-proj dgrad, consumed in the GEMM epilogue by swiglu_backward:
+                // d_gate|d_up + their absmax written directly (d_h never reaches HBM)
+                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wcodes[l * 4 + W_DOWN], Hh, gs + G_DR,
+                     ws + W_DOWN, EPI_SWIGLU_BWD, d_gu, F, b.gu, F, 0, 0, 0, nullptr, ga + G_DGU);
+            } else {
+                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wcodes[l * 4 + W_DOWN], Hh, gs + G_DR,
+                     ws + W_DOWN, EPI_BF16, d_h, Hh);
+                h = prof_begin();
+                QT_CHECK_K(qtk_swiglu_bwd(b.gu, d_h, M, Hh, d_gu, ga + G_DGU, st));
+                prof_end(h, 5, 2.0 * M * F * 2 + 2.0 * M * Hh);
+            }
             // ---- gate_up
             h = prof_begin();
             QT_CHECK_K(qtk_quantize_bf16(d_gu, M * F, gk, ga + G_DGU, gcodes, gs + G_DGU, st));

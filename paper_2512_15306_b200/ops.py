@@ -12,7 +12,7 @@ import torch
 from . import _lib
 
 E4M3, E5M2 = 0, 1
-EPI_BF16, EPI_F32, EPI_BF16_RES, EPI_BF16_ACC, EPI_F32_ACC = 0, 1, 2, 3, 4
+EPI_BF16, EPI_F32, EPI_BF16_RES, EPI_BF16_ACC, EPI_F32_ACC, EPI_SWIGLU_BWD = 0, 1, 2, 3, 4, 5
 
 
 def _p(t: torch.Tensor | None) -> int | None:
@@ -72,7 +72,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
          a_fmt: int = E4M3, b_fmt: int = E4M3, a_scale: torch.Tensor | None = None,
          b_scale: torch.Tensor | None = None, epi: int = EPI_BF16, out: torch.Tensor | None = None,
          res: torch.Tensor | None = None, sr: tuple[int, int, int] = (0, 0, 0), bn: int = 0,
-         a2: torch.Tensor | None = None, split_k: int = 1) -> torch.Tensor:
+         a2: torch.Tensor | None = None, split_k: int = 1, amax: torch.Tensor | None = None) -> torch.Tensor:
     """D[m,n] = sum_k A[m,k] B[n,k].  A stored [M][K] (a_mn=False) or [K][M]
     (a_mn=True); likewise B.  uint8 operands are FP8 codes, bf16 operands BF16."""
     _need_cuda(a, b)
@@ -100,6 +100,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
             ws = torch.empty(nbytes // 4, dtype=torch.float32, device=a.device)
             g.ws, g.ws_bytes = _p(ws), nbytes
     g.split_k = split_k
+    g.amax = _p(amax)
     _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
     return out
 

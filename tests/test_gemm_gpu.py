@@ -194,3 +194,25 @@ def test_fp8_gemm_splitk_wgrad(ops, ref, M, N):
     scale = _absscale(ref, ac, 1, sa, bc, 0, sb)
     _check_close(g_split.float().cpu().numpy(), want, absscale=scale, K=K, frac=0.99)
     _check_close(g_plain.float().cpu().numpy(), want, absscale=scale, K=K, frac=0.99)
+
+
+@pytest.mark.parametrize("M,H,K", [(256, 512, 256), (300, 1216, 384)])
+def test_fp8_gemm_swiglu_backward_epilogue(ops, M, H, K):
+    """Down-projection dgrad with swiglu_backward (src/tensorops.cpp:133-153) in the
+    epilogue: bitwise equal to the separate dgrad (bf16 d_h) + SwiGLU-backward kernel,
+    absmax included."""
+    g = torch.Generator(device="cpu").manual_seed(5)
+    ac = torch.randint(0, 120, (M, K), dtype=torch.uint8, generator=g).cuda()
+    bc = torch.randint(0, 120, (H, K), dtype=torch.uint8, generator=g).cuda()  # W_down codes [d][Hh]: MN-major B
+    bc = bc.t().contiguous()  # stored [K][N] for the (K,MN) dgrad layout
+    gu = (torch.randn(M, 2 * H, generator=g) * 2).to(torch.bfloat16).cuda()
+    sa, sb = torch.tensor([3.0], device="cuda"), torch.tensor([0.75], device="cuda")
+    dh = ops.gemm(ac, bc, M=M, N=H, K=K, b_mn=True, a_scale=sa, b_scale=sb, epi=ops.EPI_BF16)
+    want, slot = ops.swiglu_bwd(gu, dh)
+    got = torch.empty(M, 2 * H, dtype=torch.bfloat16, device="cuda")
+    amax = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ops.gemm(ac, bc, M=M, N=H, K=K, b_mn=True, a_scale=sa, b_scale=sb, epi=ops.EPI_SWIGLU_BWD, out=got, res=gu,
+             amax=amax)
+    torch.cuda.synchronize()
+    assert torch.equal(got.view(torch.int16), want.view(torch.int16))
+    assert amax.item() == slot.item()
