@@ -298,6 +298,20 @@ def main():
         roof = {"kernel": dom_name, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "peak_basis": f"measured copy [{peaks['src']}]",
                 "launches": dom["launches"], "share_of_step": dom["ms"] / total_ms, "traffic": None}
+    # DRAM bytes per launch of the dominant class from the committed ncu capture of one step
+    # (scripts/traffic_summary.py; cold-cache serialised replay), when it matches this config
+    tf = ROOT / "profiles" / "r01_traffic_0.5b.json"
+    if args.config == "qwen2.5-0.5b" and B == 16 and tf.exists():
+        try:
+            t = json.loads(tf.read_text())["classes"].get(dom_name)
+            if t:
+                per_call = t["dram_bytes_per_launch"] * t["launches"] / max(dom["launches"], 1)
+                roof["traffic"] = per_call
+                roof["traffic_unit"] = "bytes/launch (dram read+write, ncu)"
+                roof["algorithmic_per_launch"] = dom["work"] / max(dom["launches"], 1)
+                roof["traffic_source"] = str(tf.relative_to(ROOT))
+        except Exception:
+            pass
     classes = {k: {"ms": round(v["ms"], 3), "launches": v["launches"],
                    ("tflops" if k.startswith(("gemm", "attn")) else "gbs"):
                        round(v["work"] / (v["ms"] / 1e3) / (1e12 if k.startswith(("gemm", "attn")) else 1e9), 1)}
