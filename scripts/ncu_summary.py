@@ -20,5 +20,5 @@ for f in sorted(sys.argv[1:] or glob.glob("gpurun_out/ncu/*.raw.csv")):
         rb, wb = d["dram__bytes_read.sum"], d["dram__bytes_write.sum"]
         print(f"{str(d['Kernel Name'])[:48]:48s} grid={str(d.get('Grid Size',''))[:14]:14s} t={t*1e6:9.1f}us "
               f"rd={rb/1e6:9.1f}MB wr={wb/1e6:9.1f}MB {(rb+wb)/t/1e9:7.0f}GB/s sm%={d['sm__throughput.avg.pct_of_peak_sustained_elapsed']:5.1f} "
-              f"mem%={d['gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed']:5.1f} tc%={d.get('sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active', 0):6.3f} "
+              f"mem%={d['gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed']:5.1f} tensor%={d.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active', 0) or 0:5.1f} "
               f"warps%={d['sm__warps_active.avg.pct_of_peak_sustained_active']:5.1f} regs={d['launch__registers_per_thread']:.0f}")
