@@ -89,6 +89,12 @@ typedef struct QtkGemm {
     int64_t ws_bytes;
     int split_k;        /* 0 = auto (only when the tile grid starves the SMs), 1 = off     */
     uint32_t* amax;     /* EPI_SWIGLU_BWD: absmax (u32 |x| bits) of the output              */
+    /* EPI_F32 logits only (all three set or all NULL): per-row softmax statistics of   */
+    /* each 128-column block, (max, sum exp(x - max)) as float pairs [M][ceil(N/128)], */
+    /* and the logit at column ce_targets[row] -> ce_tgt_logit[row]                     */
+    const int32_t* ce_targets;
+    float* ce_stats;
+    float* ce_tgt_logit;
 } QtkGemm;
 
 int qtk_gemm(const QtkGemm* g, cudaStream_t s);
@@ -158,6 +164,11 @@ int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t 
  * written as bf16 hi + lo parts (either may be NULL). */
 int qtk_ce_softmax(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets, float inv_n,
                    void* dlogits, void* dlogits_lo, int64_t ldd, float* loss_rows, cudaStream_t s);
+/* same, with the per-row statistics the logits GEMM produced (QtkGemm.ce_*): one
+ * pass over the logits instead of two */
+int qtk_ce_softmax_stats(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets,
+                         const float* stats, const float* tgt_logit, float inv_n, void* dlogits, void* dlogits_lo,
+                         int64_t ldd, float* loss_rows, cudaStream_t s);
 int qtk_loss_reduce(const float* loss_rows, int64_t n, float inv_n, float* out, float* accum, cudaStream_t s);
 
 /* optimizer (src/optim.cpp:37-110).  segs: device array of per-tensor segment

@@ -24,6 +24,7 @@ class QtkGemm(C.Structure):
         ("epi", C.c_int), ("out", c_vp), ("ldo", c_i64), ("res", c_vp), ("ldr", c_i64),
         ("sr_seed", c_u64), ("sr_stream", c_u64), ("sr_base", c_u64), ("bn", C.c_int), ("a2", c_vp),
         ("ws", c_vp), ("ws_bytes", c_i64), ("split_k", C.c_int), ("amax", c_vp),
+        ("ce_targets", c_vp), ("ce_stats", c_vp), ("ce_tgt_logit", c_vp),
     ]
 
 
@@ -36,6 +37,8 @@ _SIGS = {
     "qtk_gemm": (C.c_int, [C.POINTER(QtkGemm), c_vp]),
     "qtk_gemm_splitk_ws_bytes": (C.c_int, [c_i64, c_i64, c_i64, C.c_int]),
     "qtk_ce_softmax": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "qtk_ce_softmax_stats": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp,
+                                       c_vp]),
     "qtk_attn_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_i64, c_vp, c_vp,
                                c_vp, c_vp]),
     "qtk_attn_bwd": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -406,6 +406,65 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
     if (seg_amax && amax) atomicMax(&seg_amax[ch.seg], amax);
 }
 
+
+// Single-pass CE softmax from the logits GEMM's per-row statistics: the row's
+// (max, sum exp) is combined from its 128-column blocks, then one pass writes
+// dlogits = (exp(l - mx) / denom - [target]) / N as bf16 hi + lo
+// (tensorops.cpp:372-393); loss = mx + log(denom) - l[target].
+__global__ void __launch_bounds__(CE_T) ce_softmax_stats_kernel(const float* __restrict__ logits, int64_t ldl, int V,
+                                                                const int32_t* __restrict__ targets,
+                                                                const float2* __restrict__ stats, int nstat,
+                                                                const float* __restrict__ tgt_logit, float inv_n,
+                                                                uint16_t* __restrict__ dlogits,
+                                                                uint16_t* __restrict__ dlogits_lo, int64_t ldd,
+                                                                float* __restrict__ loss_rows) {
+    __shared__ float red[CE_T / 32];
+    const int64_t row = blockIdx.x;
+    const float2* st = stats + row * nstat;
+    float mx = -INFINITY;
+    for (int i = threadIdx.x; i < nstat; i += CE_T) mx = fmaxf(mx, st[i].x);
+    mx = block_reduce_max(mx, red);
+    float s = 0.0f;
+    for (int i = threadIdx.x; i < nstat; i += CE_T) {
+        const float2 v = st[i];
+        if (v.x != -INFINITY) s += v.y * expf(v.x - mx);
+    }
+    const float denom = block_reduce_sum(s, red);
+    const int tgt = targets[row];
+    if (threadIdx.x == 0) loss_rows[row] = (mx + logf(denom)) - tgt_logit[row];
+    if (!dlogits) return;
+    const float inv_denom = 1.0f / denom;
+    const float* l = logits + row * ldl;
+    const float4* l4 = reinterpret_cast<const float4*>(l);
+    const int V4 = V / 4;
+    uint16_t* dl = dlogits + row * ldd;
+    uint16_t* dlo = dlogits_lo ? dlogits_lo + row * ldd : nullptr;
+    for (int i = threadIdx.x; i < V4; i += CE_T) {
+        const float4 v = __ldcs(l4 + i);
+        float p[4] = {expf(v.x - mx) * inv_denom, expf(v.y - mx) * inv_denom, expf(v.z - mx) * inv_denom,
+                      expf(v.w - mx) * inv_denom};
+        float hi[4], lo[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (4 * i + j == tgt) p[j] -= 1.0f;
+            p[j] *= inv_n;
+            hi[j] = bf16r(p[j]);
+            lo[j] = p[j] - hi[j];
+        }
+        *reinterpret_cast<uint2*>(dl + 4 * i) = make_uint2(pack_bf16x2(hi[0], hi[1]), pack_bf16x2(hi[2], hi[3]));
+        if (dlo)
+            *reinterpret_cast<uint2*>(dlo + 4 * i) = make_uint2(pack_bf16x2(lo[0], lo[1]), pack_bf16x2(lo[2], lo[3]));
+    }
+    for (int i = V4 * 4 + threadIdx.x; i < V; i += CE_T) {
+        float p = expf(l[i] - mx) * inv_denom;
+        if (i == tgt) p -= 1.0f;
+        p *= inv_n;
+        const float hi = bf16r(p);
+        dl[i] = f2bfbits(hi);
+        if (dlo) dlo[i] = f2bfbits(p - hi);
+    }
+}
+
 }  // namespace qtb
 
 using namespace qtb;
@@ -418,6 +477,17 @@ int qtk_ce_softmax(const float* logits, int64_t ldl, int64_t rows, int V, const 
     if ((ldl & 3) || (dlogits && (ldd & 3))) return 1;
     ce_softmax_kernel<<<(unsigned)rows, CE_T, 0, s>>>(logits, ldl, V, targets, inv_n, (uint16_t*)dlogits,
                                                       (uint16_t*)dlogits_lo, ldd, loss_rows);
+    return (int)cudaGetLastError();
+}
+
+int qtk_ce_softmax_stats(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets,
+                         const float* stats, const float* tgt_logit, float inv_n, void* dlogits, void* dlogits_lo,
+                         int64_t ldd, float* loss_rows, cudaStream_t s) {
+    if (rows <= 0) return 0;
+    if ((ldl & 3) || (dlogits && (ldd & 3)) || !stats || !tgt_logit) return 1;
+    ce_softmax_stats_kernel<<<(unsigned)rows, CE_T, 0, s>>>(logits, ldl, V, targets, (const float2*)stats,
+                                                            (int)ceil_div(V, 128), tgt_logit, inv_n,
+                                                            (uint16_t*)dlogits, (uint16_t*)dlogits_lo, ldd, loss_rows);
     return (int)cudaGetLastError();
 }
 

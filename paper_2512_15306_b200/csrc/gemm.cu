@@ -43,6 +43,10 @@ struct alignas(64) Params {
     CUtensorMap tr;   // EPI_BF16_RES residual map
     int tma_out;      // epilogue stages tiles through smem and stores them with TMA
     uint32_t* amax;   // EPI_SWIGLU_BWD: absmax of the output
+    const int32_t* ce_targets;  // EPI_F32 logits: per-row softmax statistics (see QtkGemm)
+    float2* ce_stats;
+    float* ce_tgt_logit;
+    int ce_nstat;
     int n_fast;       // tile order: N-tiles of one M panel adjacent (they share the A panel in L2)
     int M, N, K;
     int num_m, num_n, num_k;
@@ -112,6 +116,12 @@ __device__ __forceinline__ void load_bf16x32(const uint16_t* src, float (&v)[32]
 // FMA residual x - q*d is exact, and one correction q + res*rcp rounds to the
 // correctly rounded quotient (Markstein's theorem) -- the same bits as the
 // reference's f32 division acc / denom (src/tensorops.cpp:55) in 3 instructions.
+__device__ __forceinline__ float exp2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ float div_exact(float x, float d, float rcp) {
     const float q = __fmul_rn(x, rcp);
     const float e = __fmaf_rn(-q, d, x);
@@ -220,6 +230,11 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
         ephase ^= 1;
     }
     uint32_t smax = 0;
+    // EPI_F32 logits: online (max, sum exp) of this thread's row over its BNt columns
+    const bool stats = EPI == EPI_F32 && p.ce_stats != nullptr;
+    float cm = -INFINITY, cs = 0.0f;
+    int ctgt = -1;
+    if (EPI == EPI_F32 && stats && row < p.M) ctgt = p.ce_targets[row];
     for (int g = 0; g < BNt / GC; ++g) {
         const int col0 = n0 + g * GC;
         if (col0 >= p.N) break;
@@ -250,6 +265,31 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
         if constexpr (EPI == EPI_F32 || EPI == EPI_F32_ACC) {
 #pragma unroll
             for (int j = 0; j < GC; ++j) v[j] = __uint_as_float(r[j]);
+            if (EPI == EPI_F32 && stats) {
+                constexpr float L2E = 1.4426950408889634f;
+                const int nv = min(GC, p.N - col0);
+                float gm = -INFINITY;
+#pragma unroll
+                for (int j = 0; j < GC; ++j)
+                    if (j < nv) gm = fmaxf(gm, v[j]);
+                if (gm > cm) {
+                    cs = cm == -INFINITY ? 0.0f : cs * exp2_approx((cm - gm) * L2E);
+                    cm = gm;
+                }
+                const float mb = cm * L2E;
+                float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int j = 0; j < GC; ++j)
+                    if (j < nv) s4[j & 3] += exp2_approx(__fmaf_rn(v[j], L2E, -mb));
+                cs += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                if (ctgt >= col0 && ctgt < col0 + GC) {
+                    float tv = 0.0f;
+#pragma unroll
+                    for (int j = 0; j < GC; ++j)
+                        if (col0 + j == ctgt) tv = v[j];
+                    p.ce_tgt_logit[row] = tv;
+                }
+            }
         } else if constexpr (EPI == EPI_BF16) {
 #pragma unroll
             for (int j = 0; j < GC; ++j) v[j] = div_exact(__uint_as_float(r[j]), denom, rcp);  // rounded by the pack
@@ -339,6 +379,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
         smax = warp_max_u32(smax);
         if (lane == 0 && smax) atomicMax(p.amax, smax);
     }
+    if (EPI == EPI_F32 && stats && row < p.M && n0 < p.N) p.ce_stats[(int64_t)row * p.ce_nstat + n0 / 128] = make_float2(cm, cs);
 }
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -825,6 +866,9 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0);
     const int cg = tc.cg;
     int bn = (g->bn == 128 || g->bn == 256) ? g->bn : tc.bn;
+    const bool ce = g->ce_stats != nullptr;
+    if (ce && (g->epi != EPI_F32 || !g->ce_targets || !g->ce_tgt_logit)) return 1;
+    if (ce) bn = 256;  // one 128-column statistics block per epilogue warp half
     // FP8 MN-major B split over a CTA pair needs >= 128 N-columns per CTA
     if (cg == 2 && g->kind == 0 && g->b_mn && bn == 128) bn = 256;
     Params p;
@@ -872,7 +916,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     int splits = 1;
     // the reduce pass works on 4-column vectors with 32-bit indices
     const bool reducible = g->N % 4 == 0 && g->ldo % 4 == 0 && g->M * g->N / 4 < (int64_t(1) << 31);
-    if (g->ws && g->split_k != 1 && reducible && g->epi != EPI_SWIGLU_BWD) {
+    if (g->ws && g->split_k != 1 && reducible && g->epi != EPI_SWIGLU_BWD && !ce) {
         splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn, cg);
         if ((int64_t)splits * g->M * g->N * 4 > g->ws_bytes) splits = 1;
     }
@@ -918,7 +962,11 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
             ok = make_tmap(&p.tr, g->res, 2, ncols, g->M, g->ldr, 64, 32) == 0;
         p.tma_out = ok ? 1 : 0;
         p.amax = g->amax;
-        if (g->epi == EPI_SWIGLU_BWD && !ok) return 1;  // no direct-store variant of this epilogue
+    p.ce_targets = g->ce_targets;
+    p.ce_stats = reinterpret_cast<float2*>(g->ce_stats);
+    p.ce_tgt_logit = g->ce_tgt_logit;
+    p.ce_nstat = (int)ceil_div(g->N, 128);
+        if ((g->epi == EPI_SWIGLU_BWD || ce) && !ok) return 1;  // no direct-store variant of these epilogues
     }
     const int grid = std::min(tiles, num_sms() / cg) * cg;
     return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, cg, s);

@@ -203,6 +203,8 @@ class Session {
     uint16_t* dlogits = nullptr;
     uint16_t* dlogits_lo = nullptr;
     float* loss_rows = nullptr;
+    float* ce_stats = nullptr;   // [M][ceil(V/128)] (max, sum exp) pairs from the logits GEMM
+    float* ce_tgt = nullptr;     // [M] logit of the target
     float* dgamma_part = nullptr;
     float* dgamma = nullptr;
     float* rms_inv = nullptr;  // per-row 1/rms scratch of the forward norms
@@ -453,6 +455,8 @@ class Session {
         req(&dlogits, (size_t)M * V * 2);
         req(&dlogits_lo, (size_t)M * V * 2);
         req(&loss_rows, M * 4);
+        req(&ce_stats, (size_t)M * ceil_div(V, 128) * 8);
+        req(&ce_tgt, M * 4);
         const int nblk = qtk_rmsnorm_bwd_partials(M, d);
         req(&dgamma_part, (size_t)nblk * d * 4);
         req(&dgamma, d * 4);
@@ -615,7 +619,8 @@ class Session {
     void gemm(int kind, int afmt, int bfmt, bool a_mn, bool b_mn, int64_t M, int64_t N, int64_t K, const void* a,
               int64_t lda, const void* b, int64_t ldb, const float* as, const float* bs, int epi, void* out,
               int64_t ldo, const void* res = nullptr, int64_t ldr = 0, uint64_t sr_seed = 0, uint64_t sr_stream = 0,
-              uint64_t sr_base = 0, const void* a2 = nullptr, uint32_t* amax = nullptr) {
+              uint64_t sr_base = 0, const void* a2 = nullptr, uint32_t* amax = nullptr, const int32_t* ce_targets = nullptr,
+              float* ce_st = nullptr, float* ce_tl = nullptr) {
         QtkGemm g{};
         g.kind = kind;
         g.a_fmt = afmt;
@@ -645,12 +650,23 @@ class Session {
         g.ws_bytes = gemm_ws_bytes;
         g.split_k = 0;
         g.amax = amax;
+        g.ce_targets = ce_targets;
+        g.ce_stats = ce_st;
+        g.ce_tgt_logit = ce_tl;
         const int h = prof_begin();
         QT_CHECK_K(qtk_gemm(&g, st));
         prof_end(h, kind == 0 ? 0 : 1, 2.0 * M * N * K * (a2 ? 2 : 1));
     }
 
     int gkind() const { return prec.backward_grads == 0 ? kE4M3 : kE5M2; }
+    bool ce_stats_on() const {
+        static int f = -1;
+        if (f < 0) {
+            const char* e = getenv("QTB_CE_STATS");
+            f = e ? atoi(e) : 1;
+        }
+        return f != 0 && V % 4 == 0;  // TMA-stored f32 logits rows
+    }
     bool fuse_swiglu_bwd() const {
         static int f = -1;
         if (f < 0) {
@@ -802,11 +818,24 @@ class Session {
                                    fin_amax, st));
         prof_end(h, 4, 4.0 * M * d);
         // fused CE forward (+ dlogits for the backward): logits in f32 (tensorops.cpp:372-376)
-        gemm(1, 0, 0, false, false, M, V, d, normed_final, d, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, logits, V);
-        h = prof_begin();
-        QT_CHECK_K(qtk_ce_softmax(logits, V, M, (int)V, targets, 1.0f / (float)M, with_grads ? dlogits : nullptr,
-                                  with_grads ? dlogits_lo : nullptr, V, loss_rows, st));
-        prof_end(h, 7, (with_grads ? 10.0 : 4.0) * M * V);
+        if (ce_stats_on()) {
+            // the logits GEMM also emits per-row (max, sum exp) of each 128-column block and the
+            // target logit, so the softmax stage reads the logits once
+            gemm(1, 0, 0, false, false, M, V, d, normed_final, d, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, logits,
+                 V, nullptr, 0, 0, 0, 0, nullptr, nullptr, targets, ce_stats, ce_tgt);
+            h = prof_begin();
+            QT_CHECK_K(qtk_ce_softmax_stats(logits, V, M, (int)V, targets, ce_stats, ce_tgt, 1.0f / (float)M,
+                                            with_grads ? dlogits : nullptr, with_grads ? dlogits_lo : nullptr, V,
+                                            loss_rows, st));
+            prof_end(h, 7, (with_grads ? 8.0 : 0.0) * M * V);
+        } else {
+            gemm(1, 0, 0, false, false, M, V, d, normed_final, d, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, logits,
+                 V);
+            h = prof_begin();
+            QT_CHECK_K(qtk_ce_softmax(logits, V, M, (int)V, targets, 1.0f / (float)M, with_grads ? dlogits : nullptr,
+                                      with_grads ? dlogits_lo : nullptr, V, loss_rows, st));
+            prof_end(h, 7, (with_grads ? 10.0 : 4.0) * M * V);
+        }
         QT_CHECK_K(qtk_loss_reduce(loss_rows, M, 1.0f / (float)M, loss_dev, nullptr, st));
         have_fwd = true;
         fwd_with_grads = with_grads;

@@ -72,7 +72,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
          a_fmt: int = E4M3, b_fmt: int = E4M3, a_scale: torch.Tensor | None = None,
          b_scale: torch.Tensor | None = None, epi: int = EPI_BF16, out: torch.Tensor | None = None,
          res: torch.Tensor | None = None, sr: tuple[int, int, int] = (0, 0, 0), bn: int = 0,
-         a2: torch.Tensor | None = None, split_k: int = 1, amax: torch.Tensor | None = None) -> torch.Tensor:
+         a2: torch.Tensor | None = None, split_k: int = 1, amax: torch.Tensor | None = None,
+         ce: tuple | None = None) -> torch.Tensor:
     """D[m,n] = sum_k A[m,k] B[n,k].  A stored [M][K] (a_mn=False) or [K][M]
     (a_mn=True); likewise B.  uint8 operands are FP8 codes, bf16 operands BF16."""
     _need_cuda(a, b)
@@ -101,6 +102,8 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
             g.ws, g.ws_bytes = _p(ws), nbytes
     g.split_k = split_k
     g.amax = _p(amax)
+    if ce is not None:  # (targets, stats, tgt_logit): softmax statistics in the logits epilogue
+        g.ce_targets, g.ce_stats, g.ce_tgt_logit = _p(ce[0]), _p(ce[1]), _p(ce[2])
     _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
     return out
 
@@ -115,6 +118,18 @@ def ce_softmax(logits: torch.Tensor, targets: torch.Tensor, inv_n: float, with_g
     rc = _lib.lib().qtk_ce_softmax(_p(logits), logits.stride(0), rows, V, _p(targets), inv_n, _p(hi), _p(lo), V,
                                    _p(loss), _s())
     _lib.check(rc, "qtk_ce_softmax")
+    return loss, hi, lo
+
+
+def ce_softmax_stats(logits, targets, stats, tgt_logit, inv_n: float):
+    """ce_softmax from the statistics the logits GEMM produced (single pass over the logits)."""
+    rows, V = logits.shape
+    loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    hi = torch.empty((rows, V), dtype=torch.bfloat16, device=logits.device)
+    lo = torch.empty((rows, V), dtype=torch.bfloat16, device=logits.device)
+    rc = _lib.lib().qtk_ce_softmax_stats(_p(logits), logits.stride(0), rows, V, _p(targets), _p(stats),
+                                         _p(tgt_logit), inv_n, _p(hi), _p(lo), V, _p(loss), _s())
+    _lib.check(rc, "qtk_ce_softmax_stats")
     return loss, hi, lo
 
 

@@ -1,0 +1,8 @@
+# A/B of an env switch on the 0.5B bench: VAR=name bash scripts/gpu_ab.sh
+cd $GRAFT_REPO_ROOT
+for v in 0 1 0 1; do
+  env $VAR=$v timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --profile-json gpurun_out/ab_$v.json > /dev/null 2>&1
+  python -c "
+import json;d=json.load(open('gpurun_out/ab_$v.json'));l=d['line'];k=l['kernel_classes']
+print('$VAR=$v', round(l['value']), round(l['ms_per_step'],2), l['clocks']['sm_mhz'], {c: k[c]['ms'] for c in ('gemm_bf16','ce_softmax','gemm_fp8')})"
+done
