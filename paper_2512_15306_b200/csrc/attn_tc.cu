@@ -970,8 +970,13 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
     uint64_t* r_empty = r_full + S::NST;      // [NST]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(r_empty + S::NST);
 
-    const int qt = gridDim.z - 1 - blockIdx.z, kvh = blockIdx.x, b = blockIdx.y;  // longest CTAs first
-    const int group = H / Hkv;
+    const int qt = gridDim.z - 1 - blockIdx.z, b = blockIdx.y;  // longest CTAs first
+    // blockIdx.x = (kv head, slice of its GQA group): the group's query heads may be
+    // split over gridDim.x / Hkv CTAs (dQ of a head needs no cross-head reduction)
+    const int hsplit = gridDim.x / Hkv;
+    const int kvh = blockIdx.x / hsplit;
+    const int group = (H / Hkv) / hsplit;  // query heads handled by this CTA
+    const int hbase = kvh * (H / Hkv) + (blockIdx.x % hsplit) * group;
     const int d = H * HD;
     const int per_head = qt + 1;
     const int niter = group * per_head;
@@ -1016,7 +1021,7 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
                 const int slot = hh % S::QS;
                 mbar_wait(&qo_empty[slot], ((hh / S::QS) & 1) ^ 1);
                 mbar_arrive_expect_tx(&qo_full[slot], 2 * S::TILE);
-                const int h = kvh * group + hh;
+                const int h = hbase + hh;
                 for (int c = 0; c < HD / 64; ++c) {
                     tma_load_2d(&tq, &qo_full[slot], sm + S::OFF_A + slot * S::TILE + c * 128 * 128, h * HD + c * 64, qrow);
                     tma_load_2d(&tdo, &qo_full[slot], sm + S::OFF_B + slot * S::TILE + c * 128 * 128, h * HD + c * 64,
@@ -1087,7 +1092,7 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
         const int64_t grow = (int64_t)b * T + q;
         int t = 0;
         for (int hh = 0; hh < group; ++hh) {
-            const int h = kvh * group + hh;
+            const int h = hbase + hh;
             const float Lq = qok ? lse[((int64_t)b * H + h) * T + q] : 0.0f;
             const float Dq = qok ? Dv[((int64_t)b * H + h) * T + q] : 0.0f;
             const float nl = -Lq * LOG2E, dsc = Dq * inv_sqrt_d;
@@ -1211,13 +1216,19 @@ extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* 
     if (rc) return rc;
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     dim3 grid(Hkv, B, (unsigned)ceil_div(T, 128));
+    static int dq_split = -1;
+    if (dq_split < 0) {
+        const char* e = getenv("QTB_DQ_SPLIT");
+        dq_split = e ? atoi(e) : 0;  // per-head dQ CTAs measured slower (lost K/V tile reuse across the group)
+    }
+    dim3 gdq(dq_split ? H : Hkv, B, (unsigned)ceil_div(T, 128));  // dQ: one query head per CTA
 #define QTB_BWD_TC(HD)                                                                                               \
     {                                                                                                              \
         const int smem = BwdSmem<HD>::BYTES;                                                                       \
         cudaFuncSetAttribute(dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
         cudaFuncSetAttribute(dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
         dkdv_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
-        dq_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
+        dq_tc_kernel<HD><<<gdq, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
     }
     if (hd == 64)
         QTB_BWD_TC(64)

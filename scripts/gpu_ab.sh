@@ -2,7 +2,5 @@
 cd $GRAFT_REPO_ROOT
 for v in 0 1 0 1; do
   env $VAR=$v timeout 900 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --profile-json gpurun_out/ab_$v.json > /dev/null 2>&1
-  python -c "
-import json;d=json.load(open('gpurun_out/ab_$v.json'));l=d['line'];k=l['kernel_classes']
-print('$VAR=$v', round(l['value']), round(l['ms_per_step'],2), l['clocks']['sm_mhz'], {c: k[c]['ms'] for c in ('gemm_bf16','ce_softmax','gemm_fp8')})"
+  python scripts/ab_line.py "$VAR=$v" gpurun_out/ab_$v.json
 done
