@@ -176,6 +176,15 @@ int qtk_loss_reduce(const float* loss_rows, int64_t n, float inv_n, float* out, 
 int qtk_seg_size(void);
 int qtk_grad_sumsq(const void* grad, int grad_f32, const void* segs, int nseg, int64_t nblk, double* partials,
                    double* scratch, double* out, cudaStream_t s);
+/* One shard of reduce_scatter_copy / reduce_scatter_oracle (src/comms.cpp:185-254,
+ * include/qtrain/comms.hpp:113-132): acc (f32, n) += the W bf16 chunks of this
+ * shard (device pointers indexed by source worker), own chunk first then ascending
+ * sources, each add stochastically rounded to bf16 with stream
+ * fnv1a64("rs/<step>/<layer>/<src>") and counter = element index (stochastic = 0:
+ * plain f32 adds).  The trainer's own gradient exchange is the ascending-rank f32
+ * sum of the session (src/trainer.cpp:90-103); this is the SR protocol's arithmetic. */
+int qtk_reduce_scatter_sr(float* acc, const void* const* srcs, int W, int self, int64_t n, int stochastic,
+                          uint64_t seed, uint64_t step, uint64_t layer, cudaStream_t s);
 int qtk_adamw_chunk_size(void);
 int qtk_adamw_chunk_entry_size(void);
 int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,

@@ -77,6 +77,8 @@ _SIGS = {
     "ref_model_time_step": (C.c_double, [vp, i32p, i64, i64, i64]),
     "ref_make_corpus": (ci, [ci, i64, ci, ci, ci, u64, i32p, i32p]),
     "ref_flops_per_token": (None, [C.POINTER(ci), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "ref_reduce_scatter_oracle": (ci, [f32p, f32p, ci, i64, ci, u64, u64, u64]),
+    "ref_reduce_scatter_copy": (ci, [f32p, f32p, ci, i64, ci, u64, u64, u64]),
 }
 
 _lib = None
@@ -392,3 +394,14 @@ class RefModel:
     def time_step(self, tokens, batch: int, step: int = 0) -> float:
         t = np.ascontiguousarray(tokens, np.int32).ravel()
         return lib().ref_model_time_step(self.h, t, t.size, batch, step)
+
+
+def reduce_scatter(chunks, acc, *, stochastic=True, seed=0, step=0, layer=0, protocol=False):
+    """reduce_scatter_oracle (or the copy protocol) of src/comms.cpp:185-254.
+    chunks: (W, W, n) -- chunks[i][j] is worker i's chunk for shard j; acc: (W, n)."""
+    c = np.ascontiguousarray(chunks, np.float32)
+    a = np.ascontiguousarray(acc, np.float32).copy()
+    W, n = a.shape
+    f = lib().ref_reduce_scatter_copy if protocol else lib().ref_reduce_scatter_oracle
+    _chk(f(c.ravel(), a.ravel(), W, n, int(stochastic), seed, step, layer))
+    return a

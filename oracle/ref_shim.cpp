@@ -17,6 +17,7 @@
 #include "qtrain/trainer.hpp"
 #include "qtrain/corpus.hpp"
 #include "qtrain/memplan.hpp"
+#include "qtrain/comms.hpp"
 
 #include <chrono>
 #include <cstring>
@@ -539,6 +540,41 @@ void ref_flops_per_token(const int* cfg7, double* fp8_flops, double* bf16_flops)
     const auto fb = flop_breakdown(cfg_of(cfg7), RecomputeSet::none(), false);
     *fp8_flops = fb.linear;
     *bf16_flops = fb.lmhead + fb.attention;
+}
+
+// reduce_scatter_oracle / reduce_scatter_copy (src/comms.cpp:185-254): chunks is
+// W x W x n (chunks[i][j] = worker i's chunk for shard j), acc W x n in/out
+static int rs_common(const float* chunks, float* acc, int W, std::int64_t n, int stochastic, std::uint64_t seed,
+                     std::uint64_t step, std::uint64_t layer, int protocol) {
+    return guard([&] {
+        std::vector<std::vector<Tensor>> ch((std::size_t)W);
+        std::vector<Tensor> ac;
+        for (int i = 0; i < W; ++i) {
+            for (int j = 0; j < W; ++j) ch[(std::size_t)i].push_back(make_tensor(chunks + ((std::int64_t)i * W + j) * n, {n}));
+            ac.push_back(make_tensor(acc + (std::int64_t)i * n, {n}));
+        }
+        SrSpec sr;
+        sr.stochastic = stochastic != 0;
+        sr.seed = seed;
+        sr.step = step;
+        sr.layer = layer;
+        std::vector<Tensor> out;
+        if (protocol) {
+            WorkerGroup g(W);
+            out = reduce_scatter_copy(g, ch, ac, sr, false, 0);
+        } else {
+            out = reduce_scatter_oracle(ch, ac, sr);
+        }
+        for (int i = 0; i < W; ++i) put(out[(std::size_t)i], acc + (std::int64_t)i * n);
+    });
+}
+int ref_reduce_scatter_oracle(const float* chunks, float* acc, int W, std::int64_t n, int stochastic,
+                              std::uint64_t seed, std::uint64_t step, std::uint64_t layer) {
+    return rs_common(chunks, acc, W, n, stochastic, seed, step, layer, 0);
+}
+int ref_reduce_scatter_copy(const float* chunks, float* acc, int W, std::int64_t n, int stochastic,
+                            std::uint64_t seed, std::uint64_t step, std::uint64_t layer) {
+    return rs_common(chunks, acc, W, n, stochastic, seed, step, layer, 1);
 }
 
 } // extern "C"

@@ -37,6 +37,8 @@ _SIGS = {
     "qtk_gemm": (C.c_int, [C.POINTER(QtkGemm), c_vp]),
     "qtk_gemm_splitk_ws_bytes": (C.c_int, [c_i64, c_i64, c_i64, C.c_int]),
     "qtk_ce_softmax": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp, c_vp]),
+    "qtk_reduce_scatter_sr": (C.c_int, [c_vp, C.POINTER(c_vp), C.c_int, C.c_int, c_i64, C.c_int, c_u64, c_u64, c_u64,
+                                        c_vp]),
     "qtk_ce_softmax_stats": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp,
                                        c_vp]),
     "qtk_attn_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_i64, c_vp, c_vp,

@@ -119,6 +119,27 @@ __global__ void ordered_sum_kernel(const uint16_t* __restrict__ recv, int W, int
     }
 }
 
+// reduce_scatter_copy's arithmetic (src/comms.cpp:136-146, 233-254) for one shard:
+// acc += own chunk first, then the other sources in ascending order, each add
+// SR-rounded to bf16 with stream fnv1a64("rs/<step>/<layer>/<src>"), counter = i
+// (stochastic = 0: plain f32 adds).  Source chunks are bf16.
+struct RsArgs {
+    const uint16_t* src[16];
+    uint64_t key[16];
+};
+__global__ void reduce_scatter_sr_kernel(float* __restrict__ acc, RsArgs a, int W, int self, int64_t n,
+                                         int stochastic) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float v = acc[i];
+        for (int t = 0; t < W; ++t) {
+            const int src = t == 0 ? self : (t - 1 < self ? t - 1 : t);
+            v = __fadd_rn(v, bfbits2f(a.src[src][i]));
+            if (stochastic) v = sr_bf16k(v, a.key[src], (uint64_t)i);
+        }
+        acc[i] = v;
+    }
+}
+
 inline int grid_for(int64_t n, int per = 256) { return (int)std::min<int64_t>(std::max<int64_t>(ceil_div(n, per), 1), 16 * kNumSMs); }
 
 // ---------------------------------------------------------------------------
@@ -1428,6 +1449,23 @@ int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_wo
 }
 
 uint64_t qt_fnv1a64(const char* s) { return fnv1a64(s); }
+
+// one shard of reduce_scatter_copy / reduce_scatter_oracle (src/comms.cpp:185-254):
+// srcs = W device pointers (bf16 chunks of this shard, indexed by source worker)
+int qtk_reduce_scatter_sr(float* acc, const void* const* srcs, int W, int self, int64_t n, int stochastic,
+                          uint64_t seed, uint64_t step, uint64_t layer, cudaStream_t s) {
+    if (W < 1 || W > 16 || self < 0 || self >= W || n < 0 || !acc || !srcs) return 1;
+    if (n == 0) return 0;
+    qtb::RsArgs a{};
+    for (int w = 0; w < W; ++w) {
+        if (!srcs[w]) return 1;
+        a.src[w] = static_cast<const uint16_t*>(srcs[w]);
+        const std::string name = "rs/" + std::to_string(step) + "/" + std::to_string(layer) + "/" + std::to_string(w);
+        a.key[w] = qtb::rng_key(seed, qtb::fnv1a64(name));
+    }
+    qtb::reduce_scatter_sr_kernel<<<qtb::grid_for(n), 256, 0, s>>>(acc, a, W, self, n, stochastic);
+    return (int)cudaGetLastError();
+}
 
 // Exact count of this library's kernel launches in one trainer step: the
 // step is captured into a CUDA graph (not executed) and its kernel nodes are

@@ -66,3 +66,25 @@ def test_nonfinite_gradient_raises():
     s = _session()
     with pytest.raises(S.QtError, match="non-finite gradient"):
         s.adamw_step(float("inf"))
+
+
+@pytest.mark.parametrize("W", [2, 3, 5])
+@pytest.mark.parametrize("stochastic", [True, False])
+def test_reduce_scatter_sr_matches_reference(ref, W, stochastic):
+    """qtk_reduce_scatter_sr == reduce_scatter_oracle (src/comms.cpp:233-254),
+    every shard, bit for bit."""
+    import ctypes as C
+    from paper_2512_15306_b200 import _lib
+    from tests.helpers import bf16_grid_round, rng_floats
+    n = 3001
+    chunks = bf16_grid_round(rng_floats(40 + W, W * W * n, -1, 1)).reshape(W, W, n)
+    acc = bf16_grid_round(rng_floats(50 + W, W * n, -0.5, 0.5)).reshape(W, n)
+    want = ref.reduce_scatter(chunks, acc, stochastic=stochastic, seed=7, step=5, layer=2)
+    dev_chunks = torch.from_numpy(chunks).cuda().to(torch.bfloat16)
+    for w in range(W):
+        a = torch.from_numpy(acc[w].copy()).cuda()
+        srcs = (C.c_void_p * W)(*[dev_chunks[i, w].data_ptr() for i in range(W)])
+        rc = _lib.lib().qtk_reduce_scatter_sr(a.data_ptr(), srcs, W, w, n, int(stochastic), 7, 5, 2,
+                                              torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        np.testing.assert_array_equal(a.cpu().numpy(), want[w])

@@ -240,3 +240,17 @@ def test_zero1_sharded_adamw_is_bitwise_unsharded(port):
                 part = port.adamw_tensor("w", p, z, z, g, seed=1, lo=lo, hi=hi)[0]
                 out[lo:hi] = part[lo:hi]
         _eq(out, full)
+
+
+@pytest.mark.parametrize("W", [2, 3, 4])
+def test_reference_reduce_scatter_protocol_equals_oracle(ref, W):
+    """The reference's copy-engine protocol (src/comms.cpp:185-229) and its
+    straight-summation oracle (:233-254) agree bitwise (SR and f32 modes) -- the
+    contract qtk_reduce_scatter_sr is checked against on the GPU."""
+    n = 1000
+    chunks = bf16_grid_round(rng_floats(70 + W, W * W * n, -1, 1)).reshape(W, W, n)
+    acc = bf16_grid_round(rng_floats(80 + W, W * n, -0.5, 0.5)).reshape(W, n)
+    for sto in (True, False):
+        a = ref.reduce_scatter(chunks, acc, stochastic=sto, seed=9, step=3, layer=1)
+        b = ref.reduce_scatter(chunks, acc, stochastic=sto, seed=9, step=3, layer=1, protocol=True)
+        np.testing.assert_array_equal(a, b)
