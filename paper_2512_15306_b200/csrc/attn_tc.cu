@@ -624,6 +624,308 @@ __global__ void __launch_bounds__(NT, 1) fwd1_tc_kernel(const __grid_constant__ 
     }
 }
 
+
+// ===========================================================================
+// Persistent one-pass forward: one CTA per SM walks the (q tile, head, batch)
+// items longest-first (item i -> q tile nq-1-i/(H*B)), keeping TMEM, barriers
+// and the K/V/S/P rings alive across items, so an item's prologue (Q load) and
+// epilogue (O drain) overlap its neighbours' MMAs and softmax instead of being
+// exposed once per CTA wave.  Extra barriers: q_empty (last S MMA of an item has
+// read Q) and o_empty (the softmax warps have drained O).
+// ===========================================================================
+template <int HD>
+__global__ void __launch_bounds__(NT, 1) fwd1p_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H,
+                                                         int Hkv, int B, float inv_sqrt_d, uint16_t* __restrict__ out,
+                                                         int64_t ldo, float* __restrict__ out32, float* __restrict__ lse,
+                                                         uint32_t* __restrict__ amax) {
+    using S = Smem<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+    uint64_t* q_full = bar + 0;
+    uint64_t* k_full = bar + 1;    // [2]
+    uint64_t* k_empty = bar + 3;   // [2]
+    uint64_t* v_full = bar + 5;    // [2]
+    uint64_t* v_empty = bar + 7;   // [2]
+    uint64_t* s_full = bar + 9;    // [2]
+    uint64_t* s_empty = bar + 11;  // [2]
+    uint64_t* p_full = bar + 13;   // [2]
+    uint64_t* p_empty = bar + 15;  // [2]
+    uint64_t* o_full = bar + 17;
+    uint64_t* q_empty = bar + 18;
+    uint64_t* o_empty = bar + 19;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 20);
+
+    const int nq = (T + BQ - 1) / BQ;
+    const int items = nq * H * B;
+    const int d = H * HD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto decode = [&](int it, int& qt, int& h, int& b) {
+        qt = nq - 1 - it / (H * B);
+        const int r = it % (H * B);
+        h = r % H;
+        b = r / H;
+    };
+
+    if (warp == 0 && lane == 0) tma_prefetch(&tm);
+    if (warp == 1 && lane == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        mbar_init(o_full, 1);
+        mbar_init(o_empty, NSW);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&s_empty[i], NSW);
+            mbar_init(&p_full[i], NSW);
+            mbar_init(&p_empty[i], 1);
+        }
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t s_base = smem_u32(sm);
+
+    if (warp == 0 && lane == 0) {
+        // ===== TMA producer =====
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        int n_it = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+            int qt, h, b;
+            decode(it, qt, h, b);
+            const int kvh = h / (H / Hkv);
+            if (n_it > 0) mbar_wait(q_empty, (n_it - 1) & 1);  // previous item's S MMAs have read Q
+            mbar_arrive_expect_tx(q_full, S::Q);
+            for (int c = 0; c < HD / 64; ++c)
+                tma_load_2d(&tm, q_full, sm + S::OFF_Q + c * BQ * 128, h * HD + c * 64, b * T + qt * BQ);
+            for (int j = 0; j <= qt; ++j) {
+                const int krow = b * T + j * BKV;
+                mbar_wait(&k_empty[ks], kph ^ 1);
+                mbar_arrive_expect_tx(&k_full[ks], S::K);
+                for (int c = 0; c < HD / 64; ++c)
+                    tma_load_2d(&tm, &k_full[ks], sm + S::OFF_K + ks * S::K + c * BKV * 128, d + kvh * HD + c * 64, krow);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+                mbar_wait(&v_empty[vs], vph ^ 1);
+                mbar_arrive_expect_tx(&v_full[vs], S::V);
+                for (int c = 0; c < HD / 64; ++c)
+                    tma_load_2d(&tm, &v_full[vs], sm + S::OFF_V + vs * S::V + c * BKV * 128,
+                                d + Hkv * HD + kvh * HD + c * 64, krow);
+                if (++vs == S::NVS) { vs = 0; vph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        const uint32_t idesc_s = make_idesc(1, 1, false, false, BQ, BKV);
+        const uint32_t idesc_o = make_idesc(1, 1, false, true, BQ, HD);
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        int sc = 0, pc = 0;  // S tiles / P tiles issued so far (all items)
+        int n_it = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+            int qt, h, b;
+            decode(it, qt, h, b);
+            const int nj = qt + 1;
+            mbar_wait(q_full, n_it & 1);
+            int s_issued = 0;
+            auto issue_s = [&]() {
+                mbar_wait(&k_full[ks], kph);
+                const int sb = sc & 1;
+                mbar_wait(&s_empty[sb], ((sc >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t qa = s_base + S::OFF_Q, ka = s_base + S::OFF_K + ks * S::K;
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk)
+                    mma_bf16_ss(tmem + sb * BKV, kdesc(qa, kk, BQ * 128), kdesc(ka, kk, BKV * 128), idesc_s, kk > 0);
+                tc_commit(&k_empty[ks]);
+                tc_commit(&s_full[sb]);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+                ++sc;
+                if (++s_issued == nj) tc_commit(q_empty);  // Q no longer read by this item
+            };
+            issue_s();
+            if (n_it > 0) mbar_wait(o_empty, (n_it - 1) & 1);  // previous item's O drained
+            for (int j = 0; j < nj; ++j) {
+                if (j + 1 < nj) issue_s();
+                const int pb = S::NPB == 2 ? (pc & 1) : 0;
+                const uint32_t pph = S::NPB == 2 ? ((pc >> 1) & 1) : (pc & 1);
+                mbar_wait(&p_full[pb], pph);
+                mbar_wait(&v_full[vs], vph);
+                tc_fence_after();
+                const uint32_t va = s_base + S::OFF_V + vs * S::V;
+                const uint32_t ph = s_base + S::OFF_PH + pb * 2 * S::P, pl = ph + S::P;
+#pragma unroll
+                for (int kk = 0; kk < BKV / 16; ++kk) {
+                    const uint64_t bd = mndesc(va, kk, BKV * 128);
+                    mma_bf16_ss(tmem + 256, kdesc(ph, kk, BQ * 128), bd, idesc_o, (j | kk) != 0);
+                    mma_bf16_ss(tmem + 256, kdesc(pl, kk, BQ * 128), bd, idesc_o, 1);
+                }
+                tc_commit(&v_empty[vs]);
+                tc_commit(&p_empty[pb]);
+                if (++vs == S::NVS) { vs = 0; vph ^= 1; }
+                ++pc;
+            }
+            tc_commit(o_full);
+        }
+    } else if (warp >= 4) {
+        // ===== softmax (see fwd1_tc_kernel) =====
+        const int wq = warp & 3, half = (warp - 4) >> 2;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
+        const uint32_t o_cols = lane_base + 256 + half * (HD / 2);
+        const int c0 = half * (BKV / 2);
+        const float a = inv_sqrt_d * LOG2E;
+        constexpr float RESCALE = 8.0f;
+        float* xch = reinterpret_cast<float*>(sm + S::OFF_BAR + 256);
+        const int pair_bar = 2 + wq;
+        int sc = 0, pc = 0;
+        int n_it = 0;
+        uint32_t mx = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+            int qt, h, b;
+            decode(it, qt, h, b);
+            const int nj = qt + 1;
+            const int q = qt * BQ + r;
+            float m = -INFINITY, l = 0.0f;
+            for (int j = 0; j < nj; ++j, ++sc, ++pc) {
+                const int sb = sc & 1;
+                mbar_wait(&s_full[sb], (sc >> 1) & 1);
+                tc_fence_after();
+                uint32_t rr[64];
+                tmem_ld32(lane_base + sb * BKV + c0, *reinterpret_cast<uint32_t(*)[32]>(&rr[0]));
+                tmem_ld32(lane_base + sb * BKV + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&rr[32]));
+                tmem_ld_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_empty[sb]);
+                const bool diag = j == qt;
+                const int kbase = j * BKV + c0;
+                float mt = -INFINITY;
+                if (diag) {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        if (kbase + i <= q) mt = fmaxf(mt, __uint_as_float(rr[i]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) mt = fmaxf(mt, __uint_as_float(rr[i]));
+                }
+                xch[half * BQ + r] = mt;
+                asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+                mt = fmaxf(mt, xch[(half ^ 1) * BQ + r]);
+                asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+                const int pb = S::NPB == 2 ? (pc & 1) : 0;
+                const uint32_t pph = S::NPB == 2 ? ((pc >> 1) & 1) : (pc & 1);
+                mbar_wait(&p_empty[pb], pph ^ 1);
+                const bool grow = mt > m && (m == -INFINITY || (mt - m) * a > RESCALE);
+                if (__any_sync(0xffffffffu, grow && m != -INFINITY)) {
+                    if (j >= 1) {  // O holds PV(..j-1) of this item: wait for PV(j-1)
+                        const int pb1 = S::NPB == 2 ? ((pc - 1) & 1) : 0;
+                        const uint32_t ph1 = S::NPB == 2 ? (((pc - 1) >> 1) & 1) : ((pc - 1) & 1);
+                        mbar_wait(&p_empty[pb1], ph1);
+                    }
+                    tc_fence_after();
+                    const float alpha = (grow && m != -INFINITY) ? ex2((m - mt) * a) : 1.0f;
+#pragma unroll
+                    for (int c = 0; c < HD / 64; ++c) {
+                        uint32_t ov[32];
+                        tmem_ld32(o_cols + c * 32, ov);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                        tmem_st32(o_cols + c * 32, ov);
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    l *= alpha;
+                }
+                if (grow) m = mt;
+                const float mb = m * a;
+                uint8_t* ph = sm + S::OFF_PH + pb * 2 * S::P + half * BQ * 128;
+                uint8_t* pl = ph + S::P;
+                uint32_t hi[32], lo[32];
+                float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int i = 0; i < 64; i += 2) {
+                    float pp[2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const bool live = !diag || (kbase + i + e <= q);
+                        pp[e] = live ? ex2(__fmaf_rn(__uint_as_float(rr[i + e]), a, -mb)) : 0.0f;
+                    }
+                    s4[(i >> 1) & 3] += pp[0] + pp[1];
+                    const float h0 = bf16r(pp[0]), h1 = bf16r(pp[1]);
+                    hi[i / 2] = pack_bf16x2(h0, h1);
+                    lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
+                }
+                l += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const int off = r * 128 + ((cc ^ (r & 7)) << 4);
+                    *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[cc * 4 + 0], hi[cc * 4 + 1], hi[cc * 4 + 2], hi[cc * 4 + 3]);
+                    *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[cc * 4 + 0], lo[cc * 4 + 1], lo[cc * 4 + 2], lo[cc * 4 + 3]);
+                }
+                fence_async_shared();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[pb]);
+            }
+            xch[half * BQ + r] = l;
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            const float lt = l + xch[(half ^ 1) * BQ + r];
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // xch reusable by the next item
+            const float inv_l = lt > 0.0f ? 1.0f / lt : 0.0f;
+            mbar_wait(o_full, n_it & 1);
+            tc_fence_after();
+            const bool valid = q < T;
+            const int64_t grow_ = (int64_t)b * T + q;
+#pragma unroll
+            for (int c = 0; c < HD / 64; ++c) {
+                const int col = half * (HD / 2) + c * 32;
+                uint32_t rr[32];
+                tmem_ld32(lane_base + 256 + col, rr);
+                tmem_ld_wait();
+                if (valid) {
+                    uint4* o16 = reinterpret_cast<uint4*>(out + grow_ * ldo + h * HD + col);
+                    float4* o32 = reinterpret_cast<float4*>(out32 + grow_ * ldo + h * HD + col);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4) {
+                        float f[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            f[e] = __uint_as_float(rr[v4 * 8 + e]) * inv_l;
+                            mx = max(mx, abs_bits(bf16r(f[e])));
+                        }
+                        o16[v4] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                             pack_bf16x2(f[6], f[7]));
+                        if (out32) {
+                            o32[2 * v4] = make_float4(f[0], f[1], f[2], f[3]);
+                            o32[2 * v4 + 1] = make_float4(f[4], f[5], f[6], f[7]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(o_empty);  // O drained: the next item's PV(0) may overwrite it
+            if (valid && half == 0) lse[((int64_t)b * H + h) * T + q] = m * inv_sqrt_d + logf(lt);
+        }
+        mx = warp_max_u32(mx);
+        if (lane == 0 && amax && mx) atomicMax(amax, mx);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ===========================================================================
 // Backward on tcgen05 (reference sdpa_chunked_backward, src/tensorops.cpp:257-303).
 //
@@ -1182,6 +1484,28 @@ extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, in
         const int smem = Smem<HDV>::BYTES;                                                                       \
         cudaFuncSetAttribute(KERNEL<HDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                    \
         KERNEL<HDV><<<grid, NT, smem, s>>>(tm, T, H, Hkv, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, amax);   \
+    }
+    static int persistent = -1;
+    if (persistent < 0) {
+        const char* e = getenv("QTB_ATTN_PERSIST");
+        persistent = e ? atoi(e) : 1;
+    }
+    if (persistent && !two_pass) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int items = (int)ceil_div(T, BQ) * H * B;
+        const unsigned pg = (unsigned)std::min(items, sms);
+#define QTB_FWDP(HDV)                                                                                            \
+        {                                                                                                          \
+            const int smem = Smem<HDV>::BYTES;                                                                     \
+            cudaFuncSetAttribute(fwd1p_tc_kernel<HDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+            fwd1p_tc_kernel<HDV><<<pg, NT, smem, s>>>(tm, T, H, Hkv, B, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, \
+                                                      amax);                                                       \
+        }
+        if (hd == 64) QTB_FWDP(64) else QTB_FWDP(128)
+#undef QTB_FWDP
+        return (int)cudaGetLastError();
     }
     if (hd == 64) {
         if (two_pass) QTB_FWD(fwd_tc_kernel, 64) else QTB_FWD(fwd1_tc_kernel, 64)
