@@ -103,6 +103,14 @@ __global__ void finalize_scale_kernel(const double* ssq, float mean_scale, float
     *norm_out = norm;
 }
 __global__ void set_scale_kernel(float* p, float v) { *p = v; }
+// w_amax[l*4 + k] = seg_amax[param index of block weight k of layer l] (k: qkv, o, gate_up, down)
+__global__ void gather_wamax_kernel(const uint32_t* __restrict__ seg_amax, uint32_t* __restrict__ w_amax, int L) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= L * 4) return;
+    const int l = i / 4, k = i % 4;
+    const int off[4] = {1, 2, 4, 5};
+    w_amax[i] = seg_amax[1 + 6 * l + off[k]];
+}
 // E4M3 scales of n tensors from their absmax bit patterns (absmax_scale, src/numerics.cpp:150-158)
 __global__ void weight_scale_kernel(const uint32_t* __restrict__ amax, float* __restrict__ scale, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -252,6 +260,8 @@ class Session {
     uint32_t* g_amax = nullptr;    // L*4
     float* g_scale = nullptr;      // L*4
     uint32_t* fin_amax = nullptr;
+    uint32_t* seg_amax = nullptr;  // per-parameter |w| max of the weights AdamW just wrote
+    bool amax_cached = false;      // seg_amax describes the current params (next build_step_context skips absmax)
     float* loss_dev = nullptr;     // per micro-batch losses (ga_steps)
     double* ssq_dev = nullptr;
     double* norm_dev = nullptr;
@@ -516,6 +526,7 @@ class Session {
         req(&g_amax, L * 16);
         req(&g_scale, L * 16);
         req(&fin_amax, 16);
+        req(&seg_amax, P.size() * 4);
         req(&loss_dev, std::max(plan.ga_steps, 1) * 4 + 16);
         req(&ssq_dev, 16);
         req(&norm_dev, 16);
@@ -750,12 +761,16 @@ class Session {
             if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight-code all-gather: ") + api.GetErrorString(r));
             return;
         }
+        if (amax_cached) {  // the absmax AdamW folded in while writing these weights
+            gather_wamax_kernel<<<(unsigned)ceil_div(L * 4, 128), 128, 0, st>>>(seg_amax, w_amax, L);
+            QT_CHECK_CUDA(cudaGetLastError());
+        }
         for (int l = 0; l < L; ++l) {
             const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
             for (int k = 0; k < 4; ++k) {
                 const ParamT& t = P[widx[k]];
                 const int h = prof_begin();
-                QT_CHECK_K(qtk_absmax_bf16(params + t.off, t.numel, w_amax + l * 4 + k, st));
+                if (!amax_cached) QT_CHECK_K(qtk_absmax_bf16(params + t.off, t.numel, w_amax + l * 4 + k, st));
                 QT_CHECK_K(qtk_quantize_bf16(params + t.off, t.numel, kE4M3, w_amax + l * 4 + k, wcodes[l * 4 + k],
                                              w_scale + l * 4 + k, st));
                 prof_end(h, 3, 3.0 * t.numel);
@@ -1043,10 +1058,17 @@ class Session {
         const void* g = world > 1 ? (const void*)gshard : (const void*)grads;
         const int64_t total = world > 1 ? shard_total : p_total;
         int h = prof_begin();
+        QT_CHECK_CUDA(cudaMemsetAsync(seg_amax, 0, P.size() * 4, st));
         QT_CHECK_K(qtk_adamw_dev(params, m32, v32, m16, v16, g, world > 1, segs_dev, chunks_dev, nchunks, hyper.lr,
                                  hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev, seed,
-                                 step, plan.bf16_moments, err_dev, nullptr, st));
+                                 step, plan.bf16_moments, err_dev, seg_amax, st));
         prof_end(h, 10, (double)total * (plan.bf16_moments ? 14.0 : 22.0));
+        amax_cached = !shard_weights();
+        if (world > 1 && amax_cached) {  // slice maxima -> tensor maxima
+            auto& api = NcclApi::get();
+            ncclResult_t r = api.AllReduce(seg_amax, seg_amax, P.size(), ncclUint32, ncclMax, comm, st);
+            if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight absmax: ") + api.GetErrorString(r));
+        }
         if (world > 1) {
             auto& api = NcclApi::get();
             h = prof_begin();
@@ -1196,6 +1218,7 @@ int qt_param_upload(qt_session* h, int i, const float* host) {
     return guard([&] {
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
+        s.amax_cached = false;
         QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, host, t.numel * 4, cudaMemcpyHostToDevice, s.st));
         f32_to_bf16_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.scratch_f32, s.params + t.off, t.numel);
         QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
@@ -1254,6 +1277,7 @@ int qt_moments_upload(qt_session* h, int i, const float* m, const float* v, int6
 int qt_init_params(qt_session* h, uint64_t seed) {
     return guard([&] {
         Session& s = *h->s;
+        s.amax_cached = false;
         const float std_ = 1.0f / std::sqrt(static_cast<float>(s.d));
         for (auto& t : s.P) {
             const bool gamma = t.shape.size() == 1;
@@ -1475,6 +1499,7 @@ int qt_count_step_kernels(qt_session* h, const int32_t* tokens_dev, int64_t toke
     return guard([&] {
         Session& s = *h->s;
         const int64_t saved_step = s.step_count;
+        const bool saved_amax = s.amax_cached;  // the captured step is not executed
         cudaGraph_t g = nullptr;
         QT_CHECK_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeRelaxed));
         try {
@@ -1482,10 +1507,13 @@ int qt_count_step_kernels(qt_session* h, const int32_t* tokens_dev, int64_t toke
         } catch (...) {
             cudaStreamEndCapture(s.st, &g);
             if (g) cudaGraphDestroy(g);
+            s.step_count = saved_step;
+            s.amax_cached = saved_amax;
             throw;
         }
         QT_CHECK_CUDA(cudaStreamEndCapture(s.st, &g));
         s.step_count = saved_step;
+        s.amax_cached = saved_amax;
         size_t n = 0;
         QT_CHECK_CUDA(cudaGraphGetNodes(g, nullptr, &n));
         std::vector<cudaGraphNode_t> nodes(n);
