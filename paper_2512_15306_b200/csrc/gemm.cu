@@ -791,7 +791,7 @@ int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, i
 struct TileCfg {
     int cg, bn;
 };
-TileCfg choose_cfg(int64_t M, int64_t N, int kind, bool b_mn) {
+TileCfg choose_cfg(int64_t M, int64_t N, int kind, bool b_mn, int64_t K = 1 << 20) {
     static int forced = -1;
     if (forced < 0) {
         const char* e = getenv("QTB_GEMM_CG");
@@ -802,6 +802,10 @@ TileCfg choose_cfg(int64_t M, int64_t N, int kind, bool b_mn) {
     const double peak = kind == 0 ? 21.6e12 : 10.9e12;  // per SM, dense
     const double l2 = 11.0e12 / sms;                   // bytes/s per SM (measured LTS cap, B300_MICROARCH.md)
     TileCfg best{1, 256};
+    // short-K FP8 GEMMs (the K = d_model linears): the pair's cluster handshakes are not
+    // amortised over a few k-blocks; single-CTA 128x256 tiles measured 15-20 % faster
+    // at K = 896 (scripts/gemm_small.py), equal at K = 1152, slower at K >= 4864
+    if (kind == 0 && K <= 1024 && N >= 256 && forced != 2) return best;
     double best_t = 1e30;
     for (int cg = 1; cg <= 2; ++cg) {
         if (forced == 1 && cg == 2) continue;
@@ -845,7 +849,7 @@ using namespace qtb;
 extern "C" int qtk_gemm_splitk_ws_bytes(int64_t M, int64_t N, int64_t K, int kind) {
     int best = 0;
     for (int bmn = 0; bmn < 2; ++bmn) {  // the bound over both operand layouts
-        const auto tc = qtb::gemm::choose_cfg(M, N, kind, bmn != 0);
+        const auto tc = qtb::gemm::choose_cfg(M, N, kind, bmn != 0, K);
         const int bn = (tc.cg == 2 && kind == 0 && bmn && tc.bn == 128) ? 256 : tc.bn;
         const int s = qtb::gemm::choose_splits(M, N, K, kind, bn, tc.cg);
         if (s > 1) best = std::max(best, (int)std::min<int64_t>((int64_t)s * M * N * 4, INT32_MAX));
@@ -863,7 +867,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         ((g->lda * elem) & 15) || ((g->ldb * elem) & 15))
         return 1;
     if (g->lda < (g->a_mn ? g->M : g->K) || g->ldb < (g->b_mn ? g->N : g->K)) return 1;
-    const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0);
+    const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0, g->K);
     const int cg = tc.cg;
     int bn = (g->bn == 128 || g->bn == 256) ? g->bn : tc.bn;
     const bool ce = g->ce_stats != nullptr;
