@@ -805,7 +805,7 @@ TileCfg choose_cfg(int64_t M, int64_t N, int kind, bool b_mn, int64_t K = 1 << 2
     // short-K FP8 GEMMs (the K = d_model linears): the pair's cluster handshakes are not
     // amortised over a few k-blocks; single-CTA 128x256 tiles measured 15-20 % faster
     // at K = 896 (scripts/gemm_small.py), equal at K = 1152, slower at K >= 4864
-    if (kind == 0 && K <= 1024 && N >= 256 && forced != 2) return best;
+    if (kind == 0 && K <= 1024 && N >= 256 && N <= 2048 && forced != 2) return best;  // wide N (gate_up): pairs win
     double best_t = 1e30;
     for (int cg = 1; cg <= 2; ++cg) {
         if (forced == 1 && cg == 2) continue;
