@@ -95,6 +95,9 @@ typedef struct QtkGemm {
     const int32_t* ce_targets;
     float* ce_stats;
     float* ce_tgt_logit;
+    /* EPI_*_ACC: when non-NULL, the SR counter base is read on the device as           */
+    /* (*sr_micro_step) * M * N instead of sr_base (CUDA-graph replay of the step)       */
+    const uint64_t* sr_micro_step;
 } QtkGemm;
 
 int qtk_gemm(const QtkGemm* g, cudaStream_t s);
@@ -136,6 +139,12 @@ int qtk_swiglu_fwd(const void* gu, int64_t rows, int H, void* h, uint32_t* amax,
 int qtk_swiglu_bwd(const void* gu, const void* dh, int64_t rows, int H, void* dgu, uint32_t* amax, cudaStream_t s);
 
 /* GradAccumulator::accumulate for an f32 gradient (src/model.cpp:455-462). */
+/* *_ms variants: base = (*micro_step_dev) * n (device-resident counter, graph replay) */
+int qtk_sr_accumulate_f32_ms(void* buf, const float* g, int64_t n, uint64_t seed, uint64_t stream,
+                             const uint64_t* micro_step_dev, cudaStream_t s);
+int qtk_embed_bwd_ms(const int32_t* sorted_pos, const int32_t* seg_off, const int32_t* seg_tok, const int* nseg_dev,
+                     int max_seg, const void* d_r, int d, int64_t numel, void* grad, uint64_t seed, uint64_t stream,
+                     const uint64_t* micro_step_dev, cudaStream_t s);
 int qtk_sr_accumulate_f32(void* buf, const float* g, int64_t n, uint64_t seed, uint64_t stream, uint64_t base,
                           cudaStream_t s);
 
@@ -191,6 +200,12 @@ int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void*
                   const void* chunks, int nchunks, float lr, float b1, float b2, float eps, float wd, float bc1,
                   float bc2, const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
                   uint32_t* seg_amax, cudaStream_t s);
+/* same, with step / bc1 / bc2 read on the device from step_dev = {int64 step; f32 bc1;
+ * f32 bc2} (CUDA-graph replay; bc1/bc2 still computed on the host with powf) */
+int qtk_adamw_dev_sd(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32,
+                     const void* segs, const void* chunks, int nchunks, float lr, float b1, float b2, float eps,
+                     float wd, float bc1, float bc2, const float* grad_scale_dev, uint64_t seed, int64_t step,
+                     int bf16_moments, int* err, uint32_t* seg_amax, const void* step_dev, cudaStream_t s);
 
 /* ------------------------------------------------------------------------- */
 /* device-resident session: the reference operator API                        */
@@ -260,6 +275,10 @@ int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_wo
 uint64_t qt_fnv1a64(const char* s);
 int qt_count_step_kernels(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch,
                           int64_t* kernels, int64_t* other_nodes);
+/* diagnostic: one trainer step captured into a CUDA graph and replayed `iters` times
+ * (same step counters each replay); mean device ms per replay -> *ms */
+int qt_time_graph_step(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch, int64_t step,
+                       int iters, float* ms);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,7 @@ class QtkGemm(C.Structure):
         ("epi", C.c_int), ("out", c_vp), ("ldo", c_i64), ("res", c_vp), ("ldr", c_i64),
         ("sr_seed", c_u64), ("sr_stream", c_u64), ("sr_base", c_u64), ("bn", C.c_int), ("a2", c_vp),
         ("ws", c_vp), ("ws_bytes", c_i64), ("split_k", C.c_int), ("amax", c_vp),
-        ("ce_targets", c_vp), ("ce_stats", c_vp), ("ce_tgt_logit", c_vp),
+        ("ce_targets", c_vp), ("ce_stats", c_vp), ("ce_tgt_logit", c_vp), ("sr_micro_step", c_vp),
     ]
 
 
@@ -39,6 +39,7 @@ _SIGS = {
     "qtk_ce_softmax": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "qtk_reduce_scatter_sr": (C.c_int, [c_vp, C.POINTER(c_vp), C.c_int, C.c_int, c_i64, C.c_int, c_u64, c_u64, c_u64,
                                         c_vp]),
+    "qt_time_graph_step": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, C.c_int, C.POINTER(C.c_float)]),
     "qtk_ce_softmax_stats": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp,
                                        c_vp]),
     "qtk_attn_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_i64, c_vp, c_vp,

@@ -247,12 +247,19 @@ __global__ void sum_f64_kernel(const double* __restrict__ in, int64_t n, double*
 // Optional per-segment absmax of the new weights (next step's FP8 weight
 // quantization, fused so the weights are not re-read).
 // ---------------------------------------------------------------------------
+// device-resident per-step values (CUDA-graph replay): the host writes them before
+// each launch; bc1 / bc2 still come from the host's powf (src/optim.cpp:63-64)
+struct AdamStepDev {
+    int64_t step;  // 1-based step being applied
+    float bc1, bc2;
+};
 struct AdamHyper {
     float lr, b1, b2, eps, wd, bc1, bc2;
     const float* grad_scale;  // device scalar (trainer clip * mean scale)
     uint64_t seed;
     int64_t step;  // 1-based step being applied
     int bf16_moments;
+    const AdamStepDev* sd;  // when set, step / bc1 / bc2 are read here
 };
 
 constexpr int ADAM_T = 256;
@@ -338,10 +345,17 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
     c.b2 = h.b2;
     c.omb1 = __fsub_rn(1.0f, h.b1);
     c.omb2 = __fsub_rn(1.0f, h.b2);
-    c.bc1 = h.bc1;
-    c.bc2 = h.bc2;
-    c.rbc1 = __frcp_rn(h.bc1);
-    c.rbc2 = __frcp_rn(h.bc2);
+    int64_t step = h.step;
+    float bc1 = h.bc1, bc2 = h.bc2;
+    if (h.sd) {
+        step = h.sd->step;
+        bc1 = h.sd->bc1;
+        bc2 = h.sd->bc2;
+    }
+    c.bc1 = bc1;
+    c.bc2 = bc2;
+    c.rbc1 = __frcp_rn(bc1);
+    c.rbc2 = __frcp_rn(bc2);
     c.eps = h.eps;
     c.wd = h.wd;
     c.lr = h.lr;
@@ -351,7 +365,7 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
     c.kv = h.bf16_moments ? rng_key(h.seed, sg.sv) : 0;
     c.bf16_moments = h.bf16_moments;
     const int64_t end = min(sg.n, ch.start + (int64_t)ADAM_CHUNK);
-    const uint64_t ctr_base = (uint64_t)(h.step - 1) * (uint64_t)sg.gnumel + (uint64_t)sg.gstart;
+    const uint64_t ctr_base = (uint64_t)(step - 1) * (uint64_t)sg.gnumel + (uint64_t)sg.gstart;
     const bool vec_ok = ((sg.off | sg.poff) & 3) == 0;
     G const* gs = grad + sg.off;
     uint16_t* ps = p + sg.poff;
@@ -519,12 +533,13 @@ int qtk_adamw_chunk_entry_size(void) { return (int)sizeof(AdamChunk); }
 
 // chunks: device table of qtk_adamw_nchunks entries {int32 seg, int32 pad, int64 start},
 // one per ADAM_CHUNK elements of every segment (built on the host)
-int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,
+int qtk_adamw_dev_sd(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,
                   const void* chunks, int nchunks, float lr, float b1, float b2, float eps, float wd, float bc1,
                   float bc2, const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
-                  uint32_t* seg_amax, cudaStream_t s) {
+                  uint32_t* seg_amax, const void* step_dev, cudaStream_t s) {
     if (nchunks <= 0) return 0;
-    AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, grad_scale_dev, seed, step, bf16_moments};
+    AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, grad_scale_dev, seed, step, bf16_moments,
+                static_cast<const AdamStepDev*>(step_dev)};
     if (grad_f32)
         adamw_kernel<float><<<nchunks, ADAM_T, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
                                                        (const float*)grad, (const Seg*)segs,
@@ -534,6 +549,14 @@ int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void*
                                                           (const uint16_t*)grad, (const Seg*)segs,
                                                           (const AdamChunk*)chunks, h, err, seg_amax);
     return (int)cudaGetLastError();
+}
+
+int qtk_adamw_dev(void* p, float* m, float* v, void* m16, void* v16, const void* grad, int grad_f32, const void* segs,
+                  const void* chunks, int nchunks, float lr, float b1, float b2, float eps, float wd, float bc1,
+                  float bc2, const float* grad_scale_dev, uint64_t seed, int64_t step, int bf16_moments, int* err,
+                  uint32_t* seg_amax, cudaStream_t s) {
+    return qtk_adamw_dev_sd(p, m, v, m16, v16, grad, grad_f32, segs, chunks, nchunks, lr, b1, b2, eps, wd, bc1, bc2,
+                            grad_scale_dev, seed, step, bf16_moments, err, seg_amax, nullptr, s);
 }
 
 }  // extern "C"

@@ -60,6 +60,7 @@ struct alignas(64) Params {
     const uint16_t* res;
     int64_t ldr;
     uint64_t sr_seed, sr_stream, sr_base;
+    const uint64_t* sr_ms;  // device micro-step: base = *sr_ms * M * N (graph replay), else sr_base
 };
 
 // CG = CTAs per MMA (tcgen05 cta_group): 2 pairs two SMs on a 256-row tile
@@ -174,7 +175,8 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
         }
     } else {  // *_ACC: GradAccumulator::accumulate fused (src/model.cpp:455-462)
         uint16_t* buf = reinterpret_cast<uint16_t*>(p.out) + (int64_t)row * p.ldo + col0;
-        const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
+        const uint64_t sb = p.sr_ms ? *p.sr_ms * (uint64_t)p.M * (uint64_t)p.N : p.sr_base;
+        const uint64_t ctr0 = sb + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
         const uint64_t key = rng_key(p.sr_seed, p.sr_stream);
         if (vec) {
             float b[32];
@@ -224,6 +226,9 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
     const int lane = threadIdx.x & 31;
     const int row = m_row0 + lane;
     const uint64_t key = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) ? rng_key(p.sr_seed, p.sr_stream) : 0;
+    const uint64_t sr_base = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) && p.sr_ms
+                                 ? *p.sr_ms * (uint64_t)p.M * (uint64_t)p.N
+                                 : p.sr_base;
     constexpr bool SWI = EPI == EPI_SWIGLU_BWD;
     if constexpr (LOADS && !SWI) {
         mbar_wait(ebar, ephase);
@@ -336,7 +341,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
             continue;
         }
         if constexpr (LOADS) {
-            const uint64_t ctr0 = p.sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
+            const uint64_t ctr0 = sr_base + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const uint4 u = rowp[c ^ (lane & 7)];
@@ -627,7 +632,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1) gemm_kernel(const __grid_cons
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int M, int N, FastDiv n4div, int epi,
                                      const float* __restrict__ a_scale, const float* __restrict__ b_scale,
                                      void* __restrict__ out, int64_t ldo, const uint16_t* __restrict__ res,
-                                     int64_t ldr, uint64_t seed, uint64_t stream, uint64_t base) {
+                                     int64_t ldr, uint64_t seed, uint64_t stream, uint64_t base,
+                                     const uint64_t* ms) {
+    if (ms) base = *ms * (uint64_t)M * (uint64_t)N;
     float denom = 1.0f;
     if (a_scale && b_scale) denom = __fmul_rn(*a_scale, *b_scale);
     const float rcp = __frcp_rn(denom);
@@ -916,6 +923,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     p.sr_seed = g->sr_seed;
     p.sr_stream = g->sr_stream;
     p.sr_base = g->sr_base;
+    p.sr_ms = g->sr_micro_step;
     const int tiles = p.num_m * p.num_n;
     int splits = 1;
     // the reduce pass works on 4-column vectors with 32-bit indices
@@ -940,7 +948,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
                                                 FastDiv((uint32_t)(g->N / 4)), g->epi,
                                                 g->a_scale, g->b_scale, g->out, g->ldo,
                                                 reinterpret_cast<const uint16_t*>(g->res), g->ldr, g->sr_seed,
-                                                g->sr_stream, g->sr_base);
+                                                g->sr_stream, g->sr_base, g->sr_micro_step);
         return (int)cudaGetLastError();
     }
     // L2-aware order: when an M panel is shared by few N tiles, run those N tiles side by side

@@ -199,6 +199,19 @@ class Session {
     std::vector<int64_t> soff_of;  // offset of each tensor's shard in the W x shard_total exchange layout
     bool comm_pending = false;
     bool exchange_in_backward = false;  // shard_grads: per-layer exchange during this backward
+    // CUDA-graph replay of the trainer step: per-step values live in a device block the
+    // host rewrites before each launch; kernels read them there while use_dev_ctr is set
+    struct StepBlockH {
+        int64_t step;  // AdamW step being applied (1-based)
+        float bc1, bc2;
+    };
+    uint8_t* step_blk = nullptr;  // StepBlockH, then ga_steps uint64 micro-steps
+    bool use_dev_ctr = false;
+    int cur_ga = 0;
+    cudaGraphExec_t gexec = nullptr;
+    int64_t g_tpm = -1, g_batch = -1;
+    float g_max_norm = 0.0f;
+    const uint64_t* ms_dev(int ga) const { return reinterpret_cast<const uint64_t*>(step_blk + 16) + ga; }
     ncclComm_t comm = nullptr;
 
     int L, d, F, Hh, H, Hkv, hd, q, T;
@@ -322,6 +335,7 @@ class Session {
         if (ev_grad) cudaEventDestroy(ev_grad);
         if (ev_comm) cudaEventDestroy(ev_comm);
         if (cst) cudaStreamDestroy(cst);
+        if (gexec) cudaGraphExecDestroy(gexec);
         if (arena) cudaFree(arena);
         if (st) cudaStreamDestroy(st);
     }
@@ -527,6 +541,7 @@ class Session {
         req(&g_scale, L * 16);
         req(&fin_amax, 16);
         req(&seg_amax, P.size() * 4);
+        req(&step_blk, 16 + 8 * (size_t)std::max(plan.ga_steps, 1));
         req(&loss_dev, std::max(plan.ga_steps, 1) * 4 + 16);
         req(&ssq_dev, 16);
         req(&norm_dev, 16);
@@ -682,6 +697,7 @@ class Session {
         g.ws_bytes = gemm_ws_bytes;
         g.split_k = 0;
         g.amax = amax;
+        if (use_dev_ctr && (epi == EPI_BF16_ACC || epi == EPI_F32_ACC)) g.sr_micro_step = ms_dev(cur_ga);
         g.ce_targets = ce_targets;
         g.ce_stats = ce_st;
         g.ce_tgt_logit = ce_tl;
@@ -978,15 +994,23 @@ class Session {
         {
             const ParamT& t = par("embed");
             h = prof_begin();
-            QT_CHECK_K(qtk_embed_bwd(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, grads + t.off, aseed, t.s_acc,
-                                     micro_step * (uint64_t)t.numel, st));
+            if (use_dev_ctr)
+                QT_CHECK_K(qtk_embed_bwd_ms(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, t.numel, grads + t.off,
+                                            aseed, t.s_acc, ms_dev(cur_ga), st));
+            else
+                QT_CHECK_K(qtk_embed_bwd(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, grads + t.off, aseed,
+                                         t.s_acc, micro_step * (uint64_t)t.numel, st));
             prof_end(h, 5, 4.0 * M * d);
         }
     }
 
     void accumulate_f32(const ParamT& t, const float* g, uint64_t micro_step) {
-        QT_CHECK_K(qtk_sr_accumulate_f32(grads + t.off, g, t.numel, seed + (uint64_t)rank, t.s_acc,
-                                         micro_step * (uint64_t)t.numel, st));
+        if (use_dev_ctr)
+            QT_CHECK_K(qtk_sr_accumulate_f32_ms(grads + t.off, g, t.numel, seed + (uint64_t)rank, t.s_acc,
+                                                ms_dev(cur_ga), st));
+        else
+            QT_CHECK_K(qtk_sr_accumulate_f32(grads + t.off, g, t.numel, seed + (uint64_t)rank, t.s_acc,
+                                             micro_step * (uint64_t)t.numel, st));
     }
 
     // ---------------- cross-rank gradient reduction (ZeRO-1) ----------------
@@ -1059,9 +1083,10 @@ class Session {
         const int64_t total = world > 1 ? shard_total : p_total;
         int h = prof_begin();
         QT_CHECK_CUDA(cudaMemsetAsync(seg_amax, 0, P.size() * 4, st));
-        QT_CHECK_K(qtk_adamw_dev(params, m32, v32, m16, v16, g, world > 1, segs_dev, chunks_dev, nchunks, hyper.lr,
-                                 hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev, seed,
-                                 step, plan.bf16_moments, err_dev, seg_amax, st));
+        QT_CHECK_K(qtk_adamw_dev_sd(params, m32, v32, m16, v16, g, world > 1, segs_dev, chunks_dev, nchunks, hyper.lr,
+                                    hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev,
+                                    seed, step, plan.bf16_moments, err_dev, seg_amax, use_dev_ctr ? step_blk : nullptr,
+                                    st));
         prof_end(h, 10, (double)total * (plan.bf16_moments ? 14.0 : 22.0));
         amax_cached = !shard_weights();
         if (world > 1 && amax_cached) {  // slice maxima -> tensor maxima
@@ -1087,7 +1112,72 @@ class Session {
     }
 
     // ---------------- one trainer step (src/trainer.cpp:64-110) ----------------
+    static bool graph_enabled() {
+        static int f = -1;
+        if (f < 0) {
+            const char* e = getenv("QTB_GRAPH");
+            f = e ? atoi(e) : 1;
+        }
+        return f != 0;
+    }
+
+    // One trainer step.  Steady state (weight absmax cached by the previous AdamW, no
+    // profiling): the step is captured once into a CUDA graph reading its per-step values
+    // (micro-steps, AdamW step and bias corrections) from step_blk, then replayed.
     void train_step(const int32_t* tokens, int64_t tokens_per_mb, int64_t batch, int64_t step, float max_norm) {
+        const int GA = plan.ga_steps;
+        if (!graph_enabled() || prof_on || !amax_cached) {
+            train_step_body(tokens, tokens_per_mb, batch, step, max_norm);
+            return;
+        }
+        const int64_t ntok = (int64_t)GA * tokens_per_mb;
+        if (ntok > (int64_t)GA * plan.micro_batch * (T + 1)) throw QtError(1, "train_step: token buffer too small");
+        if (tokens != tok_buf)
+            QT_CHECK_CUDA(cudaMemcpyAsync(tok_buf, tokens, ntok * 4, cudaMemcpyDeviceToDevice, st));
+        std::vector<uint8_t> blk(16 + 8 * (size_t)GA);
+        StepBlockH h{step + 1, 1.0f - std::pow(hyper.beta1, static_cast<float>(step + 1)),
+                     1.0f - std::pow(hyper.beta2, static_cast<float>(step + 1))};
+        std::memcpy(blk.data(), &h, sizeof(h));
+        for (int ga = 0; ga < GA; ++ga) {
+            const uint64_t ms = (uint64_t)step * GA + ga;
+            std::memcpy(blk.data() + 16 + 8 * ga, &ms, 8);
+        }
+        QT_CHECK_CUDA(cudaMemcpyAsync(step_blk, blk.data(), blk.size(), cudaMemcpyHostToDevice, st));
+        if (!gexec || g_tpm != tokens_per_mb || g_batch != batch || g_max_norm != max_norm) {
+            if (gexec) cudaGraphExecDestroy(gexec);
+            gexec = nullptr;
+            cudaGraph_t g = nullptr;
+            QT_CHECK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+            use_dev_ctr = true;
+            try {
+                train_step_body(tok_buf, tokens_per_mb, batch, step, max_norm);
+            } catch (...) {
+                use_dev_ctr = false;
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            use_dev_ctr = false;
+            QT_CHECK_CUDA(cudaStreamEndCapture(st, &g));
+            QT_CHECK_CUDA(cudaGraphInstantiate(&gexec, g, 0));
+            cudaGraphDestroy(g);
+            g_tpm = tokens_per_mb;
+            g_batch = batch;
+            g_max_norm = max_norm;
+        } else {
+            // host-side effects of the body (forward/backward bookkeeping, optimizer step count)
+            curB = (int)batch;
+            curT = (int)(tokens_per_mb / batch - 1);
+            curM = (int64_t)curB * curT;
+            have_fwd = true;
+            fwd_with_grads = true;
+            step_count = step + 1;
+            amax_cached = !shard_weights();
+        }
+        QT_CHECK_CUDA(cudaGraphLaunch(gexec, st));
+    }
+
+    void train_step_body(const int32_t* tokens, int64_t tokens_per_mb, int64_t batch, int64_t step, float max_norm) {
         const int GA = plan.ga_steps;
         build_step_context();
         QT_CHECK_CUDA(cudaMemsetAsync(grads, 0, p_total * 2, st));
@@ -1097,6 +1187,7 @@ class Session {
             // shard_grads: the final gradients of layer l are exchanged while layers < l run
             // backward (last micro-batch only, so the summation order stays trainer.cpp:90-103)
             exchange_in_backward = shard_grads() && ga == GA - 1;
+            cur_ga = ga;
             backward((uint64_t)step * GA + ga);
             exchange_in_backward = false;
         }
@@ -1494,6 +1585,48 @@ int qtk_reduce_scatter_sr(float* acc, const void* const* srcs, int W, int self, 
 // Exact count of this library's kernel launches in one trainer step: the
 // step is captured into a CUDA graph (not executed) and its kernel nodes are
 // counted.  Collective nodes (NCCL) are counted separately.
+// Diagnostic: one trainer step captured into a CUDA graph and replayed `iters`
+// times (the same step counters each replay, so the math repeats step `step`);
+// returns the mean device time per replay.  Measures what graph launch would
+// save over stream launch; not a training entry point.
+int qt_time_graph_step(qt_session* h, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch, int64_t step,
+                       int iters, float* ms_out) {
+    return guard([&] {
+        Session& s = *h->s;
+        const int64_t saved_step = s.step_count;
+        const bool saved_amax = s.amax_cached;
+        cudaGraph_t g = nullptr;
+        QT_CHECK_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeRelaxed));
+        try {
+            s.train_step_body(tokens_dev, tokens_per_mb, batch, step, s.hyper.max_grad_norm);
+        } catch (...) {
+            cudaStreamEndCapture(s.st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        QT_CHECK_CUDA(cudaStreamEndCapture(s.st, &g));
+        s.step_count = saved_step;
+        s.amax_cached = saved_amax;
+        cudaGraphExec_t ge = nullptr;
+        QT_CHECK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        QT_CHECK_CUDA(cudaGraphLaunch(ge, s.st));  // warm-up
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s.st);
+        for (int i = 0; i < iters; ++i) QT_CHECK_CUDA(cudaGraphLaunch(ge, s.st));
+        cudaEventRecord(b, s.st);
+        QT_CHECK_CUDA(cudaEventSynchronize(b));
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, a, b);
+        *ms_out = ms / iters;
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+    });
+}
+
 int qt_count_step_kernels(qt_session* h, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch,
                           int64_t* kernels, int64_t* other_nodes) {
     return guard([&] {
@@ -1503,7 +1636,7 @@ int qt_count_step_kernels(qt_session* h, const int32_t* tokens_dev, int64_t toke
         cudaGraph_t g = nullptr;
         QT_CHECK_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeRelaxed));
         try {
-            s.train_step(tokens_dev, tokens_per_mb, batch, saved_step, s.hyper.max_grad_norm);
+            s.train_step_body(tokens_dev, tokens_per_mb, batch, saved_step, s.hyper.max_grad_norm);
         } catch (...) {
             cudaStreamEndCapture(s.st, &g);
             if (g) cudaGraphDestroy(g);

@@ -270,3 +270,27 @@ def test_loss_curve_20_steps_free_running(ref):
     assert lg[0] == pytest.approx(lr[0], rel=1e-3)
     print(f"loss curve: max rel gap {got:.2e}, reference single-flip envelope {env:.2e}")
     assert got <= max(2.0 * env, 1e-3), (got, env, lg.tolist(), lr.tolist())
+
+
+def test_graph_replay_bitwise_equals_stream_launch(ref):
+    """Steady-state steps replayed from the captured CUDA graph (per-step values read
+    from the device step block) equal stream-launched steps bit for bit."""
+    from paper_2512_15306_b200 import session as S
+    cfgd = dict(SMALL)
+    cfg = S.ModelConfig(**cfgd)
+    sessions = []
+    for prof in (True, False):  # profiling forces the stream-launched body
+        s = S.Session(cfg, S.PrecisionMap(backward_grads="e5m2"), S.RunPlan(micro_batch=2), seed=77)
+        s.init_params(77)
+        s.set_profile(prof)
+        sessions.append(s)
+    for st in range(4):
+        toks = _tokens(cfg.vocab, 2, cfg.seq_len, 900 + st)
+        la, na = sessions[0].train_step(toks, 2, step=st)
+        lb, nb = sessions[1].train_step(toks, 2, step=st)
+        assert la == lb and na == nb, (st, la, lb, na, nb)
+    for n in ("embed", "layers.0.w_qkv", "layers.1.w_down", "lm_head", "final_g"):
+        np.testing.assert_array_equal(sessions[0].download(n), sessions[1].download(n), err_msg=n)
+        ma, va = sessions[0].moments(n)
+        mb, vb = sessions[1].moments(n)
+        np.testing.assert_array_equal(ma, mb, err_msg=n)
