@@ -209,6 +209,12 @@ class Session {
     bool use_dev_ctr = false;
     int cur_ga = 0;
     cudaGraphExec_t gexec = nullptr;
+    // pinned staging ring for the step block (pageable H2D copies would synchronise the
+    // stream); slot i is reused only after its copy has executed (event)
+    static constexpr int kBlkRing = 8;
+    uint8_t* blk_host = nullptr;
+    cudaEvent_t blk_ev[kBlkRing] = {};
+    int blk_slot = 0;
     int64_t g_tpm = -1, g_batch = -1;
     float g_max_norm = 0.0f;
     const uint64_t* ms_dev(int ga) const { return reinterpret_cast<const uint64_t*>(step_blk + 16) + ga; }
@@ -336,6 +342,9 @@ class Session {
         if (ev_comm) cudaEventDestroy(ev_comm);
         if (cst) cudaStreamDestroy(cst);
         if (gexec) cudaGraphExecDestroy(gexec);
+        for (auto& e : blk_ev)
+            if (e) cudaEventDestroy(e);
+        if (blk_host) cudaFreeHost(blk_host);
         if (arena) cudaFree(arena);
         if (st) cudaStreamDestroy(st);
     }
@@ -1134,15 +1143,24 @@ class Session {
         if (ntok > (int64_t)GA * plan.micro_batch * (T + 1)) throw QtError(1, "train_step: token buffer too small");
         if (tokens != tok_buf)
             QT_CHECK_CUDA(cudaMemcpyAsync(tok_buf, tokens, ntok * 4, cudaMemcpyDeviceToDevice, st));
-        std::vector<uint8_t> blk(16 + 8 * (size_t)GA);
+        const size_t bsz = 16 + 8 * (size_t)GA, bstride = (bsz + 63) & ~size_t(63);
+        if (!blk_host) {
+            QT_CHECK_CUDA(cudaMallocHost(&blk_host, bstride * kBlkRing));
+            for (auto& e : blk_ev) QT_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const int slot = blk_slot;
+        blk_slot = (blk_slot + 1) % kBlkRing;
+        QT_CHECK_CUDA(cudaEventSynchronize(blk_ev[slot]));  // its previous copy has executed
+        uint8_t* blk = blk_host + slot * bstride;
         StepBlockH h{step + 1, 1.0f - std::pow(hyper.beta1, static_cast<float>(step + 1)),
                      1.0f - std::pow(hyper.beta2, static_cast<float>(step + 1))};
-        std::memcpy(blk.data(), &h, sizeof(h));
+        std::memcpy(blk, &h, sizeof(h));
         for (int ga = 0; ga < GA; ++ga) {
             const uint64_t ms = (uint64_t)step * GA + ga;
-            std::memcpy(blk.data() + 16 + 8 * ga, &ms, 8);
+            std::memcpy(blk + 16 + 8 * ga, &ms, 8);
         }
-        QT_CHECK_CUDA(cudaMemcpyAsync(step_blk, blk.data(), blk.size(), cudaMemcpyHostToDevice, st));
+        QT_CHECK_CUDA(cudaMemcpyAsync(step_blk, blk, bsz, cudaMemcpyHostToDevice, st));
+        QT_CHECK_CUDA(cudaEventRecord(blk_ev[slot], st));
         if (!gexec || g_tpm != tokens_per_mb || g_batch != batch || g_max_norm != max_norm) {
             if (gexec) cudaGraphExecDestroy(gexec);
             gexec = nullptr;
