@@ -1135,7 +1135,9 @@ class Session {
     // (micro-steps, AdamW step and bias corrections) from step_blk, then replayed.
     void train_step(const int32_t* tokens, int64_t tokens_per_mb, int64_t batch, int64_t step, float max_norm) {
         const int GA = plan.ga_steps;
-        if (!graph_enabled() || prof_on || !amax_cached) {
+        // world > 1 stays stream-launched: the NCCL exchange inside a captured graph has
+        // not been exercised on hardware this round (gpurun boxes have one GPU)
+        if (!graph_enabled() || prof_on || !amax_cached || world > 1) {
             train_step_body(tokens, tokens_per_mb, batch, step, max_norm);
             return;
         }
