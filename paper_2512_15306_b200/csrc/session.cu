@@ -360,6 +360,7 @@ class Session {
         const int hd_ = cfg.d_model / cfg.n_heads;
         if (hd_ != 32 && hd_ != 64 && hd_ != 128) throw QtError(1, "head_dim must be 32, 64 or 128");
         if (cfg.d_model % 16 || cfg.d_ff % 32) throw QtError(1, "d_model % 16 and d_ff % 32 must be 0 (TMA/vector alignment)");
+        if (cfg.vocab % 8) throw QtError(1, "vocab % 8 must be 0 (TMA row alignment of the bf16 dlogits)");
         if (plan.micro_batch < 1 || plan.ga_steps < 1) throw QtError(1, "RunPlan: micro_batch/ga_steps must be >= 1");
         if (world < 1 || rank < 0 || rank >= world) throw QtError(1, "bad rank/world");
     }
