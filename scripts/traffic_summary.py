@@ -12,7 +12,7 @@ def klass(name):
     if m:
         return "gemm_fp8" if m.group(1) == "0" else "gemm_bf16"
     for pat, c in (("splitk_reduce", "gemm_fp8"), ("quantize|absmax", "quant"), ("rms|colsum", "rmsnorm"),
-                   ("fwd_tc_kernel|fwd1_tc|attn::fwd_kernel", "attn_fwd"), ("dq_tc|dkdv_tc|bwd_dot|bwd_dq|bwd_dkdv", "attn_bwd"),
+                   ("fwd_tc_kernel|fwd1_tc|fwd1p_tc|attn::fwd_kernel", "attn_fwd"), ("dq_tc|dkdv_tc|bwd_dot|bwd_dq|bwd_dkdv", "attn_bwd"),
                    ("ce_softmax|loss_reduce", "ce_softmax"), ("adamw", "adamw"), ("norm_partials|sum_f64", "grad_norm")):
         if re.search(pat, name):
             return c
