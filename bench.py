@@ -179,6 +179,9 @@ def main():
     ap.add_argument("--seq", type=int, default=0)
     ap.add_argument("--grads", default="e5m2", choices=["e4m3", "e5m2"])
     ap.add_argument("--recompute", default="")
+    ap.add_argument("--moments", default="f32", choices=["f32", "bf16_sr"])
+    ap.add_argument("--shard-grads", action="store_true")
+    ap.add_argument("--shard-weights", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample-tokens", type=int, default=8)
     ap.add_argument("--profile-json", default="")
@@ -209,7 +212,8 @@ def main():
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    plan = S.RunPlan(micro_batch=B, ga_steps=1, recompute=tuple(x for x in args.recompute.split(",") if x))
+    plan = S.RunPlan(micro_batch=B, ga_steps=1, recompute=tuple(x for x in args.recompute.split(",") if x),
+                     moments=args.moments, shard_grads=args.shard_grads, shard_weights=args.shard_weights)
     sess = S.Session(cfg, S.PrecisionMap(backward_grads=args.grads), plan, S.AdamWHyper(), seed=1234, rank=rank,
                      world=world, nccl_id=nccl_id, device=local)
     sess.init_params(1234)
@@ -323,7 +327,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "fp8", "data": "synthetic",
         "config": {"workload": args.config, "model": args.config, "global_batch": B * world, "micro_batch": B,
                    "seq_len": T, "parallelism": f"dp{world}" + ("+zero1" if world > 1 else ""),
-                   "grads": args.grads, "recompute": args.recompute or "none",
+                   "grads": args.grads, "recompute": args.recompute or "none", "moments": args.moments,
+                   "shard_grads": args.shard_grads, "shard_weights": args.shard_weights,
                    "l2": "activations/logits (GBs) exceed the 126 MB L2; no explicit flush"},
         "mfu": mfu,
         "mfu_basis": "reference formula (src/memplan.cpp:264-312) vs B200 dense spec 4.5 PF fp8 / 2.25 PF bf16",
