@@ -294,6 +294,7 @@ struct AdamConst {
 };
 
 // one element of src/optim.cpp:37-59; returns false for a non-finite gradient
+template <bool BF16M>
 __device__ __forceinline__ bool adam_elem(const AdamConst& c, float g, float& p, float& m, float& v, uint64_t ctr) {
     const float gi = __fmul_rn(g, c.gscale);
     const float m_new = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, gi));
@@ -302,7 +303,7 @@ __device__ __forceinline__ bool adam_elem(const AdamConst& c, float g, float& p,
     const float vhat = div_const(v_new, c.bc2, c.rbc2);
     const float upd = __fadd_rn(__fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), c.eps)), __fmul_rn(c.wd, p));
     const float p_new = __fsub_rn(p, __fmul_rn(c.lr, upd));
-    if (c.bf16_moments) {
+    if (BF16M) {
         m = sr_bf16k(m_new, c.km, ctr);
         v = sr_bf16k(v_new, c.kv, ctr);
     } else {
@@ -331,7 +332,7 @@ __device__ __forceinline__ void st4bf(uint16_t* p, int64_t i, float4 x) {
 
 // Lane t of the CTA owns 4 consecutive elements per iteration, so a warp
 // touches 128 consecutive elements of every stream (coalesced 8/16-B accesses).
-template <typename G>
+template <typename G, bool BF16M>
 __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p, float* __restrict__ m,
                                                        float* __restrict__ v, uint16_t* __restrict__ m16,
                                                        uint16_t* __restrict__ v16, const G* __restrict__ grad,
@@ -361,9 +362,9 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
     c.lr = h.lr;
     c.gscale = *h.grad_scale;
     c.kw = rng_key(h.seed, sg.sw);
-    c.km = h.bf16_moments ? rng_key(h.seed, sg.sm) : 0;
-    c.kv = h.bf16_moments ? rng_key(h.seed, sg.sv) : 0;
-    c.bf16_moments = h.bf16_moments;
+    c.km = BF16M ? rng_key(h.seed, sg.sm) : 0;
+    c.kv = BF16M ? rng_key(h.seed, sg.sv) : 0;
+    c.bf16_moments = BF16M;
     const int64_t end = min(sg.n, ch.start + (int64_t)ADAM_CHUNK);
     const uint64_t ctr_base = (uint64_t)(step - 1) * (uint64_t)sg.gnumel + (uint64_t)sg.gstart;
     const bool vec_ok = ((sg.off | sg.poff) & 3) == 0;
@@ -371,26 +372,63 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
     uint16_t* ps = p + sg.poff;
     uint32_t amax = 0;
     bool ok = true;
+    if (vec_ok && end - ch.start == ADAM_CHUNK) {
+        // full aligned chunk: 32-bit offsets from chunk-local base pointers, no bounds checks
+        const G* gc = gs + ch.start;
+        uint16_t* pc = ps + ch.start;
+        float* mc = m + sg.off + ch.start;
+        float* vc = v + sg.off + ch.start;
+        uint16_t* m16c = m16 + sg.off + ch.start;
+        uint16_t* v16c = v16 + sg.off + ch.start;
+        const uint64_t cb = ctr_base + (uint64_t)ch.start;
+#pragma unroll 2
+        for (int j = threadIdx.x * 4; j < ADAM_CHUNK; j += ADAM_T * 4) {
+            const float4 g4 = ld4g<G>(gc, j);
+            float4 p4 = ld4g<uint16_t>(pc, j);
+            float4 m4, v4;
+            if (BF16M) {
+                m4 = ld4g<uint16_t>(m16c, j);
+                v4 = ld4g<uint16_t>(v16c, j);
+            } else {
+                m4 = *reinterpret_cast<const float4*>(mc + j);
+                v4 = *reinterpret_cast<const float4*>(vc + j);
+            }
+            const uint64_t ctr = cb + (uint32_t)j;
+            ok &= adam_elem<BF16M>(c, g4.x, p4.x, m4.x, v4.x, ctr);
+            ok &= adam_elem<BF16M>(c, g4.y, p4.y, m4.y, v4.y, ctr + 1);
+            ok &= adam_elem<BF16M>(c, g4.z, p4.z, m4.z, v4.z, ctr + 2);
+            ok &= adam_elem<BF16M>(c, g4.w, p4.w, m4.w, v4.w, ctr + 3);
+            amax = max(max(max(amax, abs_bits(p4.x)), abs_bits(p4.y)), max(abs_bits(p4.z), abs_bits(p4.w)));
+            st4bf(pc, j, p4);
+            if (BF16M) {
+                st4bf(m16c, j, m4);
+                st4bf(v16c, j, v4);
+            } else {
+                *reinterpret_cast<float4*>(mc + j) = m4;
+                *reinterpret_cast<float4*>(vc + j) = v4;
+            }
+        }
+    } else
     for (int64_t j = ch.start + threadIdx.x * 4; j < end; j += ADAM_T * 4) {
         const uint64_t ctr = ctr_base + (uint64_t)j;
         if (vec_ok && j + 4 <= end) {
             const float4 g4 = ld4g<G>(gs, j);
             float4 p4 = ld4g<uint16_t>(ps, j);
             float4 m4, v4;
-            if (h.bf16_moments) {
+            if (BF16M) {
                 m4 = ld4g<uint16_t>(m16 + sg.off, j);
                 v4 = ld4g<uint16_t>(v16 + sg.off, j);
             } else {
                 m4 = *reinterpret_cast<const float4*>(m + sg.off + j);
                 v4 = *reinterpret_cast<const float4*>(v + sg.off + j);
             }
-            ok &= adam_elem(c, g4.x, p4.x, m4.x, v4.x, ctr);
-            ok &= adam_elem(c, g4.y, p4.y, m4.y, v4.y, ctr + 1);
-            ok &= adam_elem(c, g4.z, p4.z, m4.z, v4.z, ctr + 2);
-            ok &= adam_elem(c, g4.w, p4.w, m4.w, v4.w, ctr + 3);
+            ok &= adam_elem<BF16M>(c, g4.x, p4.x, m4.x, v4.x, ctr);
+            ok &= adam_elem<BF16M>(c, g4.y, p4.y, m4.y, v4.y, ctr + 1);
+            ok &= adam_elem<BF16M>(c, g4.z, p4.z, m4.z, v4.z, ctr + 2);
+            ok &= adam_elem<BF16M>(c, g4.w, p4.w, m4.w, v4.w, ctr + 3);
             amax = max(max(max(amax, abs_bits(p4.x)), abs_bits(p4.y)), max(abs_bits(p4.z), abs_bits(p4.w)));
             st4bf(ps, j, p4);
-            if (h.bf16_moments) {
+            if (BF16M) {
                 st4bf(m16 + sg.off, j, m4);
                 st4bf(v16 + sg.off, j, v4);
             } else {
@@ -401,12 +439,12 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
             for (int64_t e = j; e < min(j + 4, end); ++e) {
                 const int64_t i = sg.off + e;
                 float pe = bfbits2f(ps[e]);
-                float me = h.bf16_moments ? bfbits2f(m16[i]) : m[i];
-                float ve = h.bf16_moments ? bfbits2f(v16[i]) : v[i];
-                ok &= adam_elem(c, gval<G>(gs, e), pe, me, ve, ctr_base + (uint64_t)e);
+                float me = BF16M ? bfbits2f(m16[i]) : m[i];
+                float ve = BF16M ? bfbits2f(v16[i]) : v[i];
+                ok &= adam_elem<BF16M>(c, gval<G>(gs, e), pe, me, ve, ctr_base + (uint64_t)e);
                 amax = max(amax, abs_bits(pe));
                 ps[e] = f2bfbits(pe);
-                if (h.bf16_moments) {
+                if (BF16M) {
                     m16[i] = f2bfbits(me);
                     v16[i] = f2bfbits(ve);
                 } else {
@@ -541,13 +579,13 @@ int qtk_adamw_dev_sd(void* p, float* m, float* v, void* m16, void* v16, const vo
     AdamHyper h{lr, b1, b2, eps, wd, bc1, bc2, grad_scale_dev, seed, step, bf16_moments,
                 static_cast<const AdamStepDev*>(step_dev)};
     if (grad_f32)
-        adamw_kernel<float><<<nchunks, ADAM_T, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
-                                                       (const float*)grad, (const Seg*)segs,
-                                                       (const AdamChunk*)chunks, h, err, seg_amax);
+        (bf16_moments ? adamw_kernel<float, true> : adamw_kernel<float, false>)<<<nchunks, ADAM_T, 0, s>>>(
+            (uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16, (const float*)grad, (const Seg*)segs,
+            (const AdamChunk*)chunks, h, err, seg_amax);
     else
-        adamw_kernel<uint16_t><<<nchunks, ADAM_T, 0, s>>>((uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16,
-                                                          (const uint16_t*)grad, (const Seg*)segs,
-                                                          (const AdamChunk*)chunks, h, err, seg_amax);
+        (bf16_moments ? adamw_kernel<uint16_t, true> : adamw_kernel<uint16_t, false>)<<<nchunks, ADAM_T, 0, s>>>(
+            (uint16_t*)p, m, v, (uint16_t*)m16, (uint16_t*)v16, (const uint16_t*)grad, (const Seg*)segs,
+            (const AdamChunk*)chunks, h, err, seg_amax);
     return (int)cudaGetLastError();
 }
 
