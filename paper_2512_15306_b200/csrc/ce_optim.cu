@@ -185,39 +185,52 @@ __device__ __forceinline__ void load8<float>(const float* g, int64_t i, int64_t 
 template <typename G>
 __global__ void norm_partials_kernel(const G* __restrict__ g, const Seg* __restrict__ segs, int nseg, int64_t nblk,
                                      double* __restrict__ part) {
-    // segment starts staged once per CTA; warps grid-stride over the blocks and
-    // binary-search shared memory
+    // each warp owns a contiguous run of 256-element blocks, so the segment changes
+    // rarely along it (tracked incrementally; one binary search per warp); U blocks'
+    // loads in flight.  Per block: lane-sequential f64 squares then a fixed xor tree.
     extern __shared__ int64_t s_blk0[];
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) s_blk0[i] = segs[i].blk0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    constexpr int U = 4;  // blocks (16-B loads per lane) in flight per warp
-    for (int64_t b0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; b0 < nblk; b0 += U * nw) {
+    const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t per = (nblk + nw - 1) / nw;
+    const int64_t b_begin = w * per, b_end = min(nblk, b_begin + per);
+    if (b_begin >= b_end) return;
+    int sg = 0;
+    {
+        int lo = 0, hi = nseg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (s_blk0[mid] <= b_begin) lo = mid;
+            else hi = mid - 1;
+        }
+        sg = lo;
+    }
+    constexpr int U = 4;
+    for (int64_t b0 = b_begin; b0 < b_end; b0 += U) {
         float x[U][8];
+        int segu[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t b = b0 + u * nw;
-            if (b < nblk) {
-                int lo = 0, hi = nseg - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_blk0[mid] <= b) lo = mid;
-                    else hi = mid - 1;
-                }
-                load8<G>(g + segs[lo].off, (b - s_blk0[lo]) * 256 + lane * 8, segs[lo].n, x[u]);
+            const int64_t b = b0 + u;
+            if (b < b_end) {
+                while (sg + 1 < nseg && s_blk0[sg + 1] <= b) ++sg;
+                segu[u] = sg;
+                load8<G>(g + segs[sg].off, (b - s_blk0[sg]) * 256 + lane * 8, segs[sg].n, x[u]);
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t b = b0 + u * nw;
-            if (b >= nblk) break;
+            const int64_t b = b0 + u;
+            if (b >= b_end) break;
             double p = 0.0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) p = __dadd_rn(p, __dmul_rn((double)x[u][j], (double)x[u][j]));
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, o));
             if (lane == 0) part[b] = p;
+            (void)segu;
         }
     }
 }
