@@ -137,6 +137,11 @@ int qtk_rope(void* qkv, int64_t rows, int T, int n_rot_heads, int hd, int qkv_di
 /* swiglu_fused / swiglu_backward (src/tensorops.cpp:114-153) + fused absmax. */
 int qtk_swiglu_fwd(const void* gu, int64_t rows, int H, void* h, uint32_t* amax, cudaStream_t s);
 int qtk_swiglu_bwd(const void* gu, const void* dh, int64_t rows, int H, void* dgu, uint32_t* amax, cudaStream_t s);
+/* Test infrastructure: counts[0..2] = mismatches of the SwiGLU kernels' fast
+ * x/(1+e) and 1/(1+e) against div.rn / rcp.rn over all 65536 bf16 gate
+ * values, and how many took the fast path; counts[3..5] = a failing gate's
+ * bf16 bits and both f32 quotients (device counters, 6 x u32). */
+int qtk_swiglu_selfcheck(uint32_t* counts, cudaStream_t s);
 
 /* GradAccumulator::accumulate for an f32 gradient (src/model.cpp:455-462). */
 /* *_ms variants: base = (*micro_step_dev) * n (device-resident counter, graph replay) */

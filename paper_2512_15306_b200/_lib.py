@@ -52,6 +52,7 @@ _SIGS = {
     "qtk_rmsnorm_bwd_partials": (C.c_int, [c_i64, C.c_int]),
     "qtk_swiglu_fwd": (C.c_int, [c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp]),
     "qtk_swiglu_bwd": (C.c_int, [c_vp, c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp]),
+    "qtk_swiglu_selfcheck": (C.c_int, [c_vp, c_vp]),
     "qtk_attn_set_mode": (None, [C.c_int, C.c_int]),
     "qtk_rope": (C.c_int, [c_vp, c_i64, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, C.c_int, c_vp, c_vp]),
 }

@@ -84,6 +84,38 @@ def test_swiglu(ops, ref, rows, h):
     assert d.max() <= 1 and (d == 0).mean() > 0.999
 
 
+def test_swiglu_fast_quotient_exhaustive(ops):
+    """The SwiGLU kernels' branch-free x/(1+e) and 1/(1+e) equal div.rn / rcp.rn
+    on all 65536 bf16 gate values -- the quotient depends on nothing else, so
+    the kernels' outputs are those of the div.rn formulation for every input."""
+    from paper_2512_15306_b200 import _lib
+    c = torch.zeros(6, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().qtk_swiglu_selfcheck(c.data_ptr(), torch.cuda.current_stream().cuda_stream),
+               "qtk_swiglu_selfcheck")
+    bad_q, bad_s, fast, g_bits, q, q_ref = c.cpu().tolist()
+    assert bad_q == 0 and bad_s == 0, (bad_q, bad_s, hex(g_bits), hex(q & 0xFFFFFFFF), hex(q_ref & 0xFFFFFFFF))
+    assert fast > 35000                         # fast path: 2^-100 <= |g| <= 2^100 and 1+e <= 2^100
+
+
+def test_swiglu_special_values(ops, ref):
+    """Zeros of both signs, huge / tiny / subnormal gates (slow-path vectors) next to ordinary ones."""
+    specials = np.array([0.0, -0.0, 1e-40, -1e-40, 1e-30, -100.0, -88.5, 90.0, 3e38, -3e38, 1.0, -1.0,
+                         0.5, -0.5, 2.0, 7.0], np.float32)
+    rows, h = 6, 16
+    gu = rng_floats(11, rows * 2 * h, -4, 4).reshape(rows, 2 * h)
+    gu[0, :h] = specials
+    gu[3, :h] = specials[::-1]
+    dh = rng_floats(12, rows * h, -1, 1).reshape(rows, h)
+    gu = bf16_grid_round(gu)
+    hw, _ = ref.swiglu_fused(gu)
+    hg, _ = ops.swiglu_fwd(_bf16(gu))
+    d = _ulp(_np(hg), hw)
+    assert d.max() <= 1
+    dw = ref.swiglu_backward(gu, dh)
+    dg, _ = ops.swiglu_bwd(_bf16(gu), _bf16(dh))
+    assert _ulp(_np(dg), dw).max() <= 1
+
+
 def _qkv_np(B, T, H, Hkv, hd, seed):
     d = H * hd
     q = d + 2 * Hkv * hd
