@@ -315,6 +315,79 @@ __global__ void bwd_dot_kernel(const uint16_t* __restrict__ dout, const float* _
     }
 }
 
+// Vectorised D: G = hd/8 threads per (row, head), 8 columns each (one 16 B
+// dO load, two 16 B O loads).  The sum reproduces bwd_dot_kernel's order bit
+// for bit -- lane l of a warp sums columns l, l+32, ... from 0, then the
+// xor-16/8/4/2/1 tree -- because the first query row's dQ is exactly zero
+// only when D matches dP's rounding there (P = 1, O = V).  Column l = 8j + k
+// lives in thread j; the per-lane partials p_l (l < 32) end in threads 0..3,
+// the tree's levels 16 and 8 cross threads (shfl_down 2, 1), 4/2/1 are in-thread.
+template <int G>
+__global__ void __launch_bounds__(256) bwd_dot_vec_kernel(const uint16_t* __restrict__ dout,
+                                                          const float* __restrict__ o, int64_t ld, int T, int H,
+                                                          int64_t rows, float* __restrict__ D) {
+    constexpr int R = G / 4;  // columns per warp lane in bwd_dot_kernel (hd / 32)
+    const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const int j = threadIdx.x % G;
+    const bool live = gid < rows * H;
+    const int64_t row = live ? gid / H : 0;
+    const int h = live ? (int)(gid % H) : 0;
+    float x[8];
+    if (live) {
+        const int64_t off = row * ld + (int64_t)h * (G * 8) + j * 8;
+        const uint4 a = *reinterpret_cast<const uint4*>(dout + off);
+        const float4 b0 = *reinterpret_cast<const float4*>(o + off), b1 = *reinterpret_cast<const float4*>(o + off + 4);
+        const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            x[2 * k] = __fmul_rn(__uint_as_float(w[k] << 16), bv[2 * k]);
+            x[2 * k + 1] = __fmul_rn(__uint_as_float(w[k] & 0xFFFF0000u), bv[2 * k + 1]);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = 0.0f;
+    }
+    // p_l = ((0 + x_l) + x_{l+32}) + ... : column l + 32r sits in thread j + 4r
+    float p[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = __fadd_rn(0.0f, x[k]);
+#pragma unroll
+    for (int r = 1; r < R; ++r)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) p[k] = __fadd_rn(p[k], __shfl_down_sync(0xffffffffu, x[k], 4 * r, G));
+    // tree level 16 (p_l + p_{l+16}: thread j + 2) and 8 (thread j + 1)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = __fadd_rn(p[k], __shfl_down_sync(0xffffffffu, p[k], 2, G));
+#pragma unroll
+    for (int k = 0; k < 8; ++k) p[k] = __fadd_rn(p[k], __shfl_down_sync(0xffffffffu, p[k], 1, G));
+    // levels 4, 2, 1 inside thread 0
+#pragma unroll
+    for (int k = 0; k < 4; ++k) p[k] = __fadd_rn(p[k], p[k + 4]);
+    p[0] = __fadd_rn(p[0], p[2]);
+    p[1] = __fadd_rn(p[1], p[3]);
+    if (live && j == 0) {
+        const int64_t bb = row / T, t = row % T;
+        D[(bb * H + h) * T + t] = __fadd_rn(p[0], p[1]);
+    }
+}
+
+// D[b, h, t] = sum_c dO[row, h, c] * O[row, h, c] (row = b*T + t), f32
+void launch_bwd_dot(const uint16_t* dout, const float* o, int64_t ld, int T, int H, int hd, int64_t rows, float* D,
+                    cudaStream_t s) {
+    const bool vec = (ld % 8 == 0) && ((uintptr_t)dout % 16 == 0) && ((uintptr_t)o % 16 == 0);
+    const int64_t units = rows * H;
+    if (vec && hd == 64) {
+        bwd_dot_vec_kernel<8><<<(unsigned)ceil_div(units * 8, 256), 256, 0, s>>>(dout, o, ld, T, H, rows, D);
+    } else if (vec && hd == 128) {
+        bwd_dot_vec_kernel<16><<<(unsigned)ceil_div(units * 16, 256), 256, 0, s>>>(dout, o, ld, T, H, rows, D);
+    } else if (vec && hd == 32) {
+        bwd_dot_vec_kernel<4><<<(unsigned)ceil_div(units * 4, 256), 256, 0, s>>>(dout, o, ld, T, H, rows, D);
+    } else {
+        bwd_dot_kernel<<<(unsigned)ceil_div(units * 32, 256), 256, 0, s>>>(dout, o, ld, T, H, hd, rows, D);
+    }
+}
+
 // ===========================================================================
 // dK/dV: grid (ceil(T/64), Hkv, B); each warp owns 16 kv rows; loops over the
 // GQA group's heads and every query block at or after the kv block
@@ -700,8 +773,7 @@ int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t 
         return qtk_attn_bwd_tc(qkv, out32, dout, ldo, lse, Dv, B, T, H, Hkv, hd, qkv_dim, dqkv, ws, s);
     const float inv_sqrt_d = 1.0f / sqrtf((float)hd);
     const int64_t rows = (int64_t)B * T;
-    bwd_dot_kernel<<<(unsigned)ceil_div(rows * H * 32, 256), 256, 0, s>>>((const uint16_t*)dout, out32, ldo, T,
-                                                                         H, hd, rows, Dv);
+    launch_bwd_dot((const uint16_t*)dout, out32, ldo, T, H, hd, rows, Dv, s);
     dim3 gkv((unsigned)ceil_div(T, 64), H, B), gq((unsigned)ceil_div(T, 64), H, B);
 #define QTB_ATTN_BWD_V(HD, BQ, SP, FA)                                                                           \
     {                                                                                                             \

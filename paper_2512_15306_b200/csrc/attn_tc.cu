@@ -1518,8 +1518,8 @@ extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, in
 
 namespace qtb {
 namespace attn {
-__global__ void bwd_dot_kernel(const uint16_t* __restrict__ dout, const float* __restrict__ o, int64_t ld, int T,
-                               int H, int hd, int64_t rows, float* __restrict__ D);
+void launch_bwd_dot(const uint16_t* dout, const float* o, int64_t ld, int T, int H, int hd, int64_t rows, float* D,
+                    cudaStream_t s);
 }  // namespace attn
 }  // namespace qtb
 
@@ -1531,8 +1531,7 @@ extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* 
     (void)ws;  // dK/dV accumulate over the GQA group in TMEM: no partials
 
     const int64_t rows = (int64_t)B * T;
-    qtb::attn::bwd_dot_kernel<<<(unsigned)ceil_div(rows * H * 32, 256), 256, 0, s>>>((const uint16_t*)dout, out32,
-                                                                                     ldo, T, H, hd, rows, Dv);
+    qtb::attn::launch_bwd_dot((const uint16_t*)dout, out32, ldo, T, H, hd, rows, Dv, s);
     CUtensorMap tq, tdo;
     int rc = qtb::gemm::make_tmap(&tq, qkv, 2, (uint64_t)qkv_dim, (uint64_t)rows, (uint64_t)qkv_dim, 64, 128);
     if (rc) return rc;
