@@ -154,33 +154,55 @@ __device__ __forceinline__ float gval<float>(const float* g, int64_t i) {
 // one warp per 256-element block: lane l holds elements [8l, 8l+8) of the
 // block (16-B loads), squares in f64 (exact), lane-sequential then a fixed
 // shuffle tree -- deterministic, ~1e-16 relative to the sequential sum
+// 8 gradient values starting at i (zero past n) as raw bits, unpacked later: the
+// loads of a warp's U blocks are all issued before the first is consumed
 template <typename G>
-__device__ __forceinline__ void load8(const G* g, int64_t i, int64_t n, float (&x)[8]);
+struct Raw8;
 template <>
-__device__ __forceinline__ void load8<uint16_t>(const uint16_t* g, int64_t i, int64_t n, float (&x)[8]) {
-    if (i + 8 <= n && ((i & 7) == 0)) {
-        const uint4 u = *reinterpret_cast<const uint4*>(g + i);
+struct Raw8<uint16_t> {
+    uint4 u;
+    __device__ __forceinline__ void load(const uint16_t* g, int64_t i, int64_t n) {
+        if (i + 8 <= n && ((i & 7) == 0)) {
+            u = *reinterpret_cast<const uint4*>(g + i);
+        } else {
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t lo = (i + 2 * j < n) ? g[i + 2 * j] : 0u;
+                const uint32_t hi = (i + 2 * j + 1 < n) ? g[i + 2 * j + 1] : 0u;
+                w[j] = lo | (hi << 16);
+            }
+            u = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+    __device__ __forceinline__ void unpack(float (&x)[8]) const {
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             x[2 * j] = __uint_as_float(w[j] << 16);
             x[2 * j + 1] = __uint_as_float(w[j] & 0xFFFF0000u);
         }
-    } else {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = (i + j < n) ? bfbits2f(g[i + j]) : 0.0f;
     }
-}
+};
 template <>
-__device__ __forceinline__ void load8<float>(const float* g, int64_t i, int64_t n, float (&x)[8]) {
-    if (i + 8 <= n && ((i & 3) == 0)) {
-        const float4 a = *reinterpret_cast<const float4*>(g + i), b = *reinterpret_cast<const float4*>(g + i + 4);
-        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
-    } else {
+struct Raw8<float> {
+    float4 a, b;
+    __device__ __forceinline__ void load(const float* g, int64_t i, int64_t n) {
+        if (i + 8 <= n && ((i & 3) == 0)) {
+            a = *reinterpret_cast<const float4*>(g + i);
+            b = *reinterpret_cast<const float4*>(g + i + 4);
+        } else {
+            float x[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) x[j] = (i + j < n) ? g[i + j] : 0.0f;
+            for (int j = 0; j < 8; ++j) x[j] = (i + j < n) ? g[i + j] : 0.0f;
+            a = make_float4(x[0], x[1], x[2], x[3]);
+            b = make_float4(x[4], x[5], x[6], x[7]);
+        }
     }
-}
+    __device__ __forceinline__ void unpack(float (&x)[8]) const {
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    }
+};
 
 template <typename G>
 __global__ void norm_partials_kernel(const G* __restrict__ g, const Seg* __restrict__ segs, int nseg, int64_t nblk,
@@ -209,28 +231,27 @@ __global__ void norm_partials_kernel(const G* __restrict__ g, const Seg* __restr
     }
     constexpr int U = 4;
     for (int64_t b0 = b_begin; b0 < b_end; b0 += U) {
-        float x[U][8];
-        int segu[U];
+        Raw8<G> raw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t b = b0 + u;
             if (b < b_end) {
                 while (sg + 1 < nseg && s_blk0[sg + 1] <= b) ++sg;
-                segu[u] = sg;
-                load8<G>(g + segs[sg].off, (b - s_blk0[sg]) * 256 + lane * 8, segs[sg].n, x[u]);
+                raw[u].load(g + segs[sg].off, (b - s_blk0[sg]) * 256 + lane * 8, segs[sg].n);
             }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t b = b0 + u;
             if (b >= b_end) break;
+            float x[8];
+            raw[u].unpack(x);
             double p = 0.0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) p = __dadd_rn(p, __dmul_rn((double)x[u][j], (double)x[u][j]));
+            for (int j = 0; j < 8; ++j) p = __dadd_rn(p, __dmul_rn((double)x[j], (double)x[j]));
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) p = __dadd_rn(p, __shfl_xor_sync(0xffffffffu, p, o));
             if (lane == 0) part[b] = p;
-            (void)segu;
         }
     }
 }
