@@ -1,12 +1,13 @@
 """A/B of the fused RMSNorm kernels of two builds of the library at the 0.5B
-shape (M=16384, d=896): python scripts/rms_ab.py A.so B.so.  20 launches per
+shape (M=16384, d=896; RMS_M / RMS_D override): python scripts/rms_ab.py A.so B.so.  20 launches per
 CUDA graph, 5 interleaved rounds, median per launch; outputs compared bitwise."""
 import ctypes as C
 import sys
 
 import torch
 
-M, d = 16384, 896
+import os
+M, d = int(os.environ.get("RMS_M", 16384)), int(os.environ.get("RMS_D", 896))  # 7B: RMS_M=8192 RMS_D=4096
 libs = [C.CDLL(p) for p in sys.argv[1:]]
 bf = lambda *s: (torch.randn(*s, device="cuda") * 0.5).to(torch.bfloat16)
 nr, dy, ex, gam, res, x = bf(M, d), bf(M, d), bf(M, d), bf(d) + 1, bf(M, d), bf(M, d)
@@ -15,7 +16,20 @@ V = lambda t: C.c_void_p(t.data_ptr())
 outs, cases = [], []
 
 
+class Eager:  # RMS_EAGER=1: 20 stream launches instead of a graph replay
+    def __init__(self, fn):
+        self.fn = fn
+
+    def replay(self):
+        for _ in range(20):
+            self.fn(torch.cuda.current_stream().cuda_stream)
+
+
 def graph(fn):
+    if os.environ.get("RMS_EAGER"):
+        fn(torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        return Eager(fn)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         fn(s.cuda_stream)
