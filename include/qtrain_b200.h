@@ -249,6 +249,22 @@ int qt_nccl_unique_id(void* out128);
 int qt_session_create(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan, const QtAdamW* hyper,
                       uint64_t seed, int rank, int world, const void* nccl_id, int device, qt_session** out);
 void qt_session_destroy(qt_session* s);
+
+/* In-process worker group (the reference's WorkerGroup, include/qtrain/comms.hpp:51-78,
+ * src/comms.cpp:19-38): `world` sessions, one per host thread, on one GPU or several,
+ * created with qt_session_create_in_group(..., group, rank, device, ...).  Their
+ * collectives are copy-engine pulls between the sessions' arenas (cudaMemcpyAsync,
+ * no SM work, src/comms.cpp:185-293) ordered by CUDA events and a
+ * host barrier; every rank must enter the same collectives in the same order (as
+ * in the reference).  The group must outlive its sessions. */
+typedef struct qt_group qt_group;
+int qt_group_create(int world, qt_group** out);
+void qt_group_destroy(qt_group* g);
+int qt_session_create_in_group(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan,
+                               const QtAdamW* hyper, uint64_t seed, qt_group* group, int rank, int device,
+                               qt_session** out);
+/* "none" (world 1), "nccl" or "peer-copy" */
+const char* qt_session_transport(qt_session* s);
 void* qt_session_stream(qt_session* s);
 size_t qt_session_bytes(qt_session* s);
 int qt_num_params(qt_session* s);
@@ -278,6 +294,12 @@ int qt_set_profile(qt_session* s, int on);
 int qt_profile_read(qt_session* s, int ncat, double* ms, int64_t* launches, double* work);
 int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_worker);
 uint64_t qt_fnv1a64(const char* s);
+/* the RoPE {cos, sin} table the session builds (T x hd/2 float pairs, the
+ * reference's powf/cosf/sinf, src/model.cpp:178-183) -> host_out (T*hd floats) */
+int qt_rope_table(int T, int hd, float* host_out);
+/* which instantiation qtk_gemm launches for *g (no launch): cta_group, BN,
+ * split-K factor, grid, output tiles per CTA of the persistent loop */
+int qtk_gemm_plan(const QtkGemm* g, int* cg, int* bn, int* splits, int* grid, int* tiles_per_cta);
 int qt_count_step_kernels(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch,
                           int64_t* kernels, int64_t* other_nodes);
 /* diagnostic: one trainer step captured into a CUDA graph and replayed `iters` times

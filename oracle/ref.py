@@ -79,6 +79,7 @@ _SIGS = {
     "ref_flops_per_token": (None, [C.POINTER(ci), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "ref_reduce_scatter_oracle": (ci, [f32p, f32p, ci, i64, ci, u64, u64, u64]),
     "ref_reduce_scatter_copy": (ci, [f32p, f32p, ci, i64, ci, u64, u64, u64]),
+    "ref_rope_apply": (ci, [C.POINTER(ci), f32p, i64, i64, ci]),
 }
 
 _lib = None
@@ -244,6 +245,16 @@ def sdpa_backward(q, k, v, go, chunk_rows=0):
     dq, dk, dv = np.empty_like(q), np.empty_like(k), np.empty_like(v)
     _chk(lib().ref_sdpa_backward(q, k, v, go, H, k.shape[0], T, D, chunk_rows or T, dq, dk, dv))
     return dq, dk, dv
+
+
+def rope_apply(cfg7, qkv, batch: int, seq: int, backward: bool = False) -> np.ndarray:
+    """The reference's own rope_apply (src/model.cpp:169-191, internal to
+    model.cpp; exported by oracle/ref_internal.cpp) on a (batch*seq, qkv_dim)
+    f32 tensor; returns the rotated copy."""
+    x = _f32(qkv).copy()
+    arr = (ci * 7)(*cfg7)
+    _chk(lib().ref_rope_apply(arr, x, batch, seq, int(backward)))
+    return x
 
 
 def embedding_backward(ids, grad_out, vocab):

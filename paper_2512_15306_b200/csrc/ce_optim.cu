@@ -373,6 +373,7 @@ __global__ void __launch_bounds__(ADAM_T) adamw_kernel(uint16_t* __restrict__ p,
                                                        const Seg* __restrict__ segs,
                                                        const AdamChunk* __restrict__ chunks, AdamHyper h,
                                                        int* __restrict__ err, uint32_t* __restrict__ seg_amax) {
+    if (err && *err != 0) return;  // gated step: earlier non-finite / out-of-range error (nothing updated)
     const AdamChunk ch = chunks[blockIdx.x];
     const Seg sg = segs[ch.seg];
     AdamConst c;

@@ -774,6 +774,8 @@ int dispatch(int kind, bool a_mn, bool b_mn, int bn, int epi, const Params& p, i
     QTB_GEMM_CASE(0, false, false, EPI_BF16)
     QTB_GEMM_CASE(0, false, false, EPI_BF16_RES)
     QTB_GEMM_CASE(0, false, true, EPI_BF16)
+    QTB_GEMM_CASE(0, false, true, EPI_F32)  // split-K partials of a small-M dgrad
+    QTB_GEMM_CASE(0, false, false, EPI_F32)  // split-K partials of a small-M forward
     QTB_GEMM_CASE(0, false, true, EPI_SWIGLU_BWD)
     QTB_GEMM_CASE(0, true, true, EPI_BF16)
     QTB_GEMM_CASE(0, true, true, EPI_BF16_ACC)
@@ -864,6 +866,53 @@ extern "C" int qtk_gemm_splitk_ws_bytes(int64_t M, int64_t N, int64_t K, int kin
     return best;
 }
 
+namespace qtb {
+namespace gemm {
+// The launch decision of qtk_gemm (cta_group, BN, split-K factor), shared with
+// qtk_gemm_plan so tests can assert which instantiation a shape runs.
+struct Decision {
+    int cg, bn, splits;
+};
+Decision decide(const QtkGemm* g) {
+    const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0, g->K);
+    Decision d{tc.cg, (g->bn == 128 || g->bn == 256) ? g->bn : tc.bn, 1};
+    const bool ce = g->ce_stats != nullptr;
+    if (ce) d.bn = 256;  // one 128-column statistics block per epilogue warp half
+    // FP8 MN-major B split over a CTA pair needs >= 128 N-columns per CTA
+    if (d.cg == 2 && g->kind == 0 && g->b_mn && d.bn == 128) d.bn = 256;
+    // the reduce pass works on 4-column vectors with 32-bit indices
+    const bool reducible = g->N % 4 == 0 && g->ldo % 4 == 0 && g->M * g->N / 4 < (int64_t(1) << 31);
+    if (g->ws && g->split_k != 1 && reducible && g->epi != EPI_SWIGLU_BWD && !ce) {
+        d.splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, d.bn, d.cg);
+        if ((int64_t)d.splits * g->M * g->N * 4 > g->ws_bytes) d.splits = 1;
+    }
+    if (d.splits > 1) {
+        const int bk = g->kind == 0 ? 128 : 64;
+        const int nk = (int)ceil_div(g->K, bk);
+        d.splits = (int)ceil_div(nk, (int)ceil_div(nk, d.splits));  // no empty splits
+    }
+    return d;
+}
+}  // namespace gemm
+}  // namespace qtb
+
+// Which kernel instantiation qtk_gemm would launch for *g (no launch):
+// cta_group (1 or 2), BN (128 or 256), split-K factor, grid size (CTAs) and
+// output tiles per CTA (the persistent loop's trip count, rounded up).
+extern "C" int qtk_gemm_plan(const QtkGemm* g, int* cg, int* bn, int* splits, int* grid, int* tiles_per_cta) {
+    using namespace qtb::gemm;
+    if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 1;
+    const Decision d = decide(g);
+    const int64_t tiles = ceil_div(g->M, (int64_t)BM * d.cg) * ceil_div(g->N, (int64_t)d.bn) * d.splits;
+    const int64_t ctas = std::min<int64_t>(tiles, num_sms() / d.cg) * d.cg;
+    *cg = d.cg;
+    *bn = d.bn;
+    *splits = d.splits;
+    *grid = (int)ctas;
+    *tiles_per_cta = (int)ceil_div(tiles, ctas / d.cg);
+    return 0;
+}
+
 extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     using namespace qtb::gemm;
     if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;
@@ -874,14 +923,11 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         ((g->lda * elem) & 15) || ((g->ldb * elem) & 15))
         return 1;
     if (g->lda < (g->a_mn ? g->M : g->K) || g->ldb < (g->b_mn ? g->N : g->K)) return 1;
-    const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0, g->K);
-    const int cg = tc.cg;
-    int bn = (g->bn == 128 || g->bn == 256) ? g->bn : tc.bn;
+    const Decision dec = decide(g);
+    const int cg = dec.cg;
+    const int bn = dec.bn;
     const bool ce = g->ce_stats != nullptr;
     if (ce && (g->epi != EPI_F32 || !g->ce_targets || !g->ce_tgt_logit)) return 1;
-    if (ce) bn = 256;  // one 128-column statistics block per epilogue warp half
-    // FP8 MN-major B split over a CTA pair needs >= 128 N-columns per CTA
-    if (cg == 2 && g->kind == 0 && g->b_mn && bn == 128) bn = 256;
     Params p;
     memset(&p, 0, sizeof(p));
     int rc;
@@ -925,17 +971,11 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     p.sr_base = g->sr_base;
     p.sr_ms = g->sr_micro_step;
     const int tiles = p.num_m * p.num_n;
-    int splits = 1;
-    // the reduce pass works on 4-column vectors with 32-bit indices
-    const bool reducible = g->N % 4 == 0 && g->ldo % 4 == 0 && g->M * g->N / 4 < (int64_t(1) << 31);
-    if (g->ws && g->split_k != 1 && reducible && g->epi != EPI_SWIGLU_BWD && !ce) {
-        splits = g->split_k > 1 ? g->split_k : choose_splits(g->M, g->N, g->K, g->kind, bn, cg);
-        if ((int64_t)splits * g->M * g->N * 4 > g->ws_bytes) splits = 1;
-    }
+    const int splits = dec.splits;
     p.splits = splits;
     p.kb_per_split = (int)ceil_div(p.num_k, splits);
     if (splits > 1) {
-        p.splits = (int)ceil_div(p.num_k, p.kb_per_split);  // no empty splits
+        p.splits = (int)ceil_div(p.num_k, p.kb_per_split);  // no empty splits (== splits, see decide)
         p.out = g->ws;
         p.ldo = g->N;
         const int all = tiles * p.splits;

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "nccl_dl.h"
+#include "transport.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -95,7 +96,8 @@ __global__ void bf16_to_f32_kernel(const uint16_t* in, float* out, int64_t n) {
 // trainer.cpp:105-107 + optim.cpp:107-110: norm = sqrt(ssq)*mean_scale,
 // clip = min(1, max/norm), grad_scale = mean_scale*clip
 __global__ void finalize_scale_kernel(const double* ssq, float mean_scale, float max_norm, float* grad_scale,
-                                      double* norm_out) {
+                                      double* norm_out, int* err) {
+    if (!isfinite(*ssq) && *err == 0) *err = 3;
     const double norm = sqrt(*ssq) * (double)mean_scale;
     float clip = 1.0f;
     if (!(max_norm <= 0.0f || norm <= (double)max_norm)) clip = (float)((double)max_norm / norm);
@@ -103,6 +105,21 @@ __global__ void finalize_scale_kernel(const double* ssq, float mean_scale, float
     *norm_out = norm;
 }
 __global__ void set_scale_kernel(float* p, float v) { *p = v; }
+// Update gate (the reference throws before any update, model.cpp:125-129, 324-325):
+// an out-of-range token, a non-finite forward statistic or loss poisons the local
+// sum of squares with NaN before the cross-rank all-reduce, so every rank sees the
+// same non-finite norm and skips AdamW (adamw_kernel returns when *err != 0).
+__global__ void poison_ssq_kernel(double* ssq, const int* err, const uint32_t* act_amax, int n_act,
+                                  const uint32_t* fin_amax, const float* losses, int n_loss) {
+    bool bad = *err != 0 || *fin_amax >= 0x7F800000u;
+    for (int i = 0; i < n_act; ++i) bad |= act_amax[i] >= 0x7F800000u;
+    for (int i = 0; i < n_loss; ++i) bad |= !isfinite(losses[i]);
+    if (bad) *ssq = __longlong_as_double(0x7FF8000000000000ll);
+}
+// non-finite global norm -> err = 3 (adamw_step: non-finite gradient) unless already set
+__global__ void gate_kernel(const double* ssq, int* err) {
+    if (!isfinite(*ssq) && *err == 0) *err = 3;
+}
 // w_amax[l*4 + k] = seg_amax[param index of block weight k of layer l] (k: qkv, o, gate_up, down)
 __global__ void gather_wamax_kernel(const uint32_t* __restrict__ seg_amax, uint32_t* __restrict__ w_amax, int L) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -145,6 +162,19 @@ __global__ void reduce_scatter_sr_kernel(float* __restrict__ acc, RsArgs a, int 
             if (stochastic) v = sr_bf16k(v, a.key[src], (uint64_t)i);
         }
         acc[i] = v;
+    }
+}
+
+// rope_apply angles (src/model.cpp:178-183) with the reference's own float libm
+// calls (std::pow / std::cos / std::sin on float): T x hd/2 {cos, sin}
+void rope_table_host(int T, int hd, float2* tab) {
+    const int half = hd / 2;
+    for (int t = 0; t < T; ++t) {
+        for (int i = 0; i < half; ++i) {
+            const float freq = std::pow(10000.0f, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
+            const float angle = static_cast<float>(t) * freq;
+            tab[(size_t)t * half + i] = make_float2(std::cos(angle), std::sin(angle));
+        }
     }
 }
 
@@ -218,7 +248,7 @@ class Session {
     int64_t g_tpm = -1, g_batch = -1;
     float g_max_norm = 0.0f;
     const uint64_t* ms_dev(int ga) const { return reinterpret_cast<const uint64_t*>(step_blk + 16) + ga; }
-    ncclComm_t comm = nullptr;
+    std::unique_ptr<Transport> tr;  // world > 1: NCCL or the in-process copy-engine peer group
 
     int L, d, F, Hh, H, Hkv, hd, q, T;
     int64_t V, Mmax;
@@ -292,6 +322,8 @@ class Session {
     int curB = 0, curT = 0;
     int64_t curM = 0;
     bool have_fwd = false, fwd_with_grads = false;
+    bool in_step = false;          // inside train_step_body (per-micro-batch losses in loss_dev[1..GA])
+    int64_t pre_step_count = -1;   // step_count before the last train_step (restored when it is gated)
 
     // profiling
     bool prof_on = false;
@@ -300,7 +332,7 @@ class Session {
     size_t ev_used = 0;
 
     Session(const QtModelConfig& c, const QtPrecisionMap& p, const QtRunPlan& pl, const QtAdamW& h, uint64_t sd, int rk,
-            int ws, const void* nccl_id, int device)
+            int ws, const void* nccl_id, int device, std::shared_ptr<PeerGroup> group = nullptr)
         : cfg(c), prec(p), plan(pl), hyper(h), seed(sd), rank(rk), world(ws) {
         validate();
         QT_CHECK_CUDA(cudaSetDevice(device));
@@ -321,13 +353,17 @@ class Session {
         build_segments();
         build_rope_table();
         if (world > 1) {
-            auto& api = NcclApi::get();
-            if (!api.ok) throw QtError(3, "world > 1 needs NCCL (libnccl.so.2 not loadable)");
-            if (!nccl_id) throw QtError(1, "world > 1 needs an NCCL unique id");
-            ncclUniqueId id;
-            std::memcpy(&id, nccl_id, sizeof(id));
-            ncclResult_t r = api.CommInitRank(&comm, world, id, rank);
-            if (r != ncclSuccess) throw QtError(3, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+            try {
+                if (group) {
+                    if (group->world != world) throw QtError(1, "peer group size != world");
+                    tr = std::make_unique<PeerTransport>(group, rank, device, arena, arena_bytes);
+                } else {
+                    if (!nccl_id) throw QtError(1, "world > 1 needs an NCCL unique id (or a peer group)");
+                    tr = std::make_unique<NcclTransport>(rank, world, nccl_id);
+                }
+            } catch (const TransportError& e) {
+                throw QtError(3, e.what());
+            }
             QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
             QT_CHECK_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
             QT_CHECK_CUDA(cudaEventCreateWithFlags(&ev_comm, cudaEventDisableTiming));
@@ -336,7 +372,7 @@ class Session {
     }
 
     ~Session() {
-        if (comm) NcclApi::get().CommDestroy(comm);
+        tr.reset();
         for (auto e : ev_pool) cudaEventDestroy(e);
         if (ev_grad) cudaEventDestroy(ev_grad);
         if (ev_comm) cudaEventDestroy(ev_comm);
@@ -512,7 +548,9 @@ class Session {
         req(&loss_rows, M * 4);
         req(&ce_stats, (size_t)M * ceil_div(V, 128) * 8);
         req(&ce_tgt, M * 4);
-        const int nblk = qtk_rmsnorm_bwd_partials(M, d);
+        // the fused and streaming backward paths need different scratch; size for the worst row count
+        int nblk = 0;
+        for (int64_t r = 1; r <= M; ++r) nblk = std::max(nblk, qtk_rmsnorm_bwd_partials(r, d));
         req(&dgamma_part, (size_t)nblk * d * 4);
         req(&dgamma, d * 4);
         req(&rms_inv, M * 4);
@@ -635,17 +673,9 @@ class Session {
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
 
-    // rope_apply angles (src/model.cpp:178-183) with the reference's own float libm calls
     void build_rope_table() {
-        const int half = hd / 2;
-        std::vector<float2> tab((size_t)T * half);
-        for (int t = 0; t < T; ++t) {
-            for (int i = 0; i < half; ++i) {
-                const float freq = std::pow(10000.0f, -2.0f * static_cast<float>(i) / static_cast<float>(hd));
-                const float angle = static_cast<float>(t) * freq;
-                tab[(size_t)t * half + i] = make_float2(std::cos(angle), std::sin(angle));
-            }
-        }
+        std::vector<float2> tab((size_t)T * (hd / 2));
+        rope_table_host(T, hd, tab.data());
         QT_CHECK_CUDA(cudaMemcpyAsync(rope_tab, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
@@ -717,6 +747,15 @@ class Session {
     }
 
     int gkind() const { return prec.backward_grads == 0 ? kE4M3 : kE5M2; }
+    // a collective through the transport; its failures surface as runtime_error (status 3)
+    template <typename F>
+    void coll(F&& f) {
+        try {
+            f();
+        } catch (const TransportError& e) {
+            throw QtError(3, e.what());
+        }
+    }
     bool ce_stats_on() const {
         static int f = -1;
         if (f < 0) {
@@ -754,7 +793,6 @@ class Session {
             // the u32 |x| bit patterns), each rank casts its slice with that scale, and the
             // E4M3 codes (1 B/param, half the bf16 traffic) are all-gathered in place.
             // Codes equal a cast of the full tensor bit for bit (the cast is elementwise).
-            auto& api = NcclApi::get();
             for (int l = 0; l < L; ++l) {
                 const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
                 for (int k = 0; k < 4; ++k) {
@@ -764,11 +802,10 @@ class Session {
                     if (n > 0) QT_CHECK_K(qtk_absmax_bf16(params + t.off + lo, n, w_amax + l * 4 + k, st));
                 }
             }
-            ncclResult_t r = api.AllReduce(w_amax, w_amax, (size_t)L * 4, ncclUint32, ncclMax, comm, st);
-            if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight absmax: ") + api.GetErrorString(r));
+            coll([&] { tr->allreduce_max_u32(w_amax, (size_t)L * 4, st); });
             weight_scale_kernel<<<(unsigned)ceil_div(L * 4, 128), 128, 0, st>>>(w_amax, w_scale, L * 4);  // ranks with an empty slice
             QT_CHECK_CUDA(cudaGetLastError());
-            api.GroupStart();
+            std::vector<AllGatherItem> items;
             for (int l = 0; l < L; ++l) {
                 const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
                 for (int k = 0; k < 4; ++k) {
@@ -780,11 +817,10 @@ class Session {
                         QT_CHECK_K(qtk_quantize_bf16(params + t.off + lo, n, kE4M3, w_amax + l * 4 + k,
                                                      wcodes[l * 4 + k] + lo, w_scale + l * 4 + k, st));
                     prof_end(h, 3, 3.0 * n);
-                    api.AllGather(wcodes[l * 4 + k] + lo, wcodes[l * 4 + k], (size_t)t.pw, ncclUint8, comm, st);
+                    items.push_back({wcodes[l * 4 + k], (size_t)t.pw});
                 }
             }
-            r = api.GroupEnd();
-            if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight-code all-gather: ") + api.GetErrorString(r));
+            coll([&] { tr->allgather(items, st); });
             return;
         }
         if (amax_cached) {  // the absmax AdamW folded in while writing these weights
@@ -1027,24 +1063,13 @@ class Session {
     // all-to-all of bf16 shards + ascending-rank f32 sum == trainer.cpp:90-103 bitwise,
     // for the tensors [i0, i1) of the parameter list, on stream s
     void reduce_tensors(int i0, int i1, cudaStream_t s) {
-        auto& api = NcclApi::get();
-        api.GroupStart();
+        std::vector<AllToAllItem> items;
         for (int i = i0; i < i1; ++i) {
             const ParamT& t = P[i];
-            const int64_t soff = soff_of[i];
-            for (int j = 0; j < world; ++j) {
-                const uint16_t* src = grads + t.off + (int64_t)j * t.pw;
-                if (j == rank) {
-                    cudaMemcpyAsync(recvbuf + (int64_t)rank * shard_total + soff, src, t.pw * 2,
-                                    cudaMemcpyDeviceToDevice, s);
-                } else {
-                    api.Send(src, (size_t)t.pw, ncclBfloat16, j, comm, s);
-                    api.Recv(recvbuf + (int64_t)j * shard_total + soff, (size_t)t.pw, ncclBfloat16, j, comm, s);
-                }
-            }
+            items.push_back({grads + t.off, (size_t)t.pw * 2, recvbuf + soff_of[i], (size_t)shard_total * 2,
+                             (size_t)t.pw * 2});
         }
-        ncclResult_t r = api.GroupEnd();
-        if (r != ncclSuccess) throw QtError(3, std::string("NCCL grad exchange: ") + api.GetErrorString(r));
+        coll([&] { tr->alltoall(items, s); });
         const int64_t n = soff_of[i1 - 1] + P[i1 - 1].pw - soff_of[i0];
         ordered_sum_kernel<<<grid_for(n), 256, 0, s>>>(recvbuf + soff_of[i0], world, n, shard_total,
                                                       gshard + soff_of[i0]);
@@ -1077,11 +1102,10 @@ class Session {
     void grad_sumsq() {
         const void* g = world > 1 ? (const void*)gshard : (const void*)grads;
         QT_CHECK_K(qtk_grad_sumsq(g, world > 1, segs_dev, nsegs, norm_blocks, norm_partials, norm_scratch, ssq_dev, st));
-        if (world > 1) {
-            auto& api = NcclApi::get();
-            ncclResult_t r = api.AllReduce(ssq_dev, ssq_dev, 1, ncclFloat64, ncclSum, comm, st);
-            if (r != ncclSuccess) throw QtError(3, std::string("NCCL norm allreduce: ") + api.GetErrorString(r));
-        }
+        poison_ssq_kernel<<<1, 1, 0, st>>>(ssq_dev, err_dev, act_amax, have_fwd ? L * 4 : 0, fin_amax, loss_dev + 1,
+                                          in_step ? plan.ga_steps : 0);
+        QT_CHECK_CUDA(cudaGetLastError());
+        if (world > 1) coll([&] { tr->allreduce_sum_f64(ssq_dev, 1, st); });
     }
 
     // AdamW on this rank's shard + all-gather of the updated bf16 params (optim.cpp:112-176)
@@ -1099,23 +1123,17 @@ class Session {
                                     st));
         prof_end(h, 10, (double)total * (plan.bf16_moments ? 14.0 : 22.0));
         amax_cached = !shard_weights();
-        if (world > 1 && amax_cached) {  // slice maxima -> tensor maxima
-            auto& api = NcclApi::get();
-            ncclResult_t r = api.AllReduce(seg_amax, seg_amax, P.size(), ncclUint32, ncclMax, comm, st);
-            if (r != ncclSuccess) throw QtError(3, std::string("NCCL weight absmax: ") + api.GetErrorString(r));
-        }
+        if (world > 1 && amax_cached)  // slice maxima -> tensor maxima
+            coll([&] { tr->allreduce_max_u32(seg_amax, P.size(), st); });
         if (world > 1) {
-            auto& api = NcclApi::get();
             h = prof_begin();
-            api.GroupStart();
+            std::vector<AllGatherItem> items;
             for (int i = 0; i < (int)P.size(); ++i) {
                 if (shard_weights() && is_block_weight(i)) continue;  // gathered as FP8 codes next step
                 const ParamT& t = P[i];
-                api.AllGather(params + t.off + (int64_t)rank * t.pw, params + t.off, (size_t)t.pw, ncclBfloat16, comm,
-                              st);
+                items.push_back({params + t.off, (size_t)t.pw * 2});
             }
-            ncclResult_t r = api.GroupEnd();
-            if (r != ncclSuccess) throw QtError(3, std::string("NCCL param all-gather: ") + api.GetErrorString(r));
+            coll([&] { tr->allgather(items, st); });
             prof_end(h, 9, 2.0 * shard_total * (world - 1));
         }
         step_count += 1;
@@ -1136,6 +1154,7 @@ class Session {
     // (micro-steps, AdamW step and bias corrections) from step_blk, then replayed.
     void train_step(const int32_t* tokens, int64_t tokens_per_mb, int64_t batch, int64_t step, float max_norm) {
         const int GA = plan.ga_steps;
+        pre_step_count = step_count;
         // world > 1 stays stream-launched: the NCCL exchange inside a captured graph has
         // not been exercised on hardware this round (gpurun boxes have one GPU)
         if (!graph_enabled() || prof_on || !amax_cached || world > 1) {
@@ -1200,6 +1219,11 @@ class Session {
 
     void train_step_body(const int32_t* tokens, int64_t tokens_per_mb, int64_t batch, int64_t step, float max_norm) {
         const int GA = plan.ga_steps;
+        struct InStep {
+            bool& f;
+            InStep(bool& x) : f(x) { f = true; }
+            ~InStep() { f = false; }
+        } in_step_guard(in_step);
         build_step_context();
         QT_CHECK_CUDA(cudaMemsetAsync(grads, 0, p_total * 2, st));
         for (int ga = 0; ga < GA; ++ga) {
@@ -1218,7 +1242,7 @@ class Session {
         }
         grad_sumsq();
         const float mean_scale = 1.0f / (static_cast<float>(GA) * world);
-        finalize_scale_kernel<<<1, 1, 0, st>>>(ssq_dev, mean_scale, max_norm, gscale_dev, norm_dev);
+        finalize_scale_kernel<<<1, 1, 0, st>>>(ssq_dev, mean_scale, max_norm, gscale_dev, norm_dev, err_dev);
         QT_CHECK_CUDA(cudaGetLastError());
         step_count = step;
         adamw(gscale_dev);
@@ -1251,8 +1275,29 @@ class Session {
         }
         if (err == 3) {
             cudaMemsetAsync(err_dev, 0, 4, st);
-            throw QtError(3, "adamw_step: non-finite gradient");
+            throw QtError(3, "adamw_step: non-finite gradient" + nonfinite_grad_name());
         }
+    }
+    // a gated step left params and moments untouched: undo its host-side bookkeeping
+    void on_gated_step() {
+        if (pre_step_count >= 0) step_count = pre_step_count;
+        amax_cached = false;
+    }
+    // " in <name>": the first tensor in update order (NamedTensors, optim.cpp:66-74) whose
+    // norm partials are non-finite (src/optim.cpp:47 names the tensor)
+    std::string nonfinite_grad_name() {
+        std::vector<double> part((size_t)norm_blocks);
+        std::vector<SegH> segs((size_t)nsegs);
+        if (norm_blocks <= 0) return "";
+        if (cudaMemcpy(part.data(), norm_partials, part.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+            cudaMemcpy(segs.data(), segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDeviceToHost) != cudaSuccess)
+            return "";
+        for (int i = 0; i < nsegs; ++i) {
+            const int64_t nb = ceil_div(segs[i].n, 256);
+            for (int64_t b = 0; b < nb; ++b)
+                if (!std::isfinite(part[(size_t)(segs[i].blk0 + b)])) return " in " + P[i].name;
+        }
+        return world > 1 ? " (on another rank)" : "";
     }
 };
 
@@ -1265,6 +1310,9 @@ using namespace qtb;
 
 struct qt_session {
     std::unique_ptr<Session> s;
+};
+struct qt_group {
+    std::shared_ptr<PeerGroup> g;  // each member session holds a reference too
 };
 
 template <typename F>
@@ -1313,6 +1361,41 @@ int qt_session_create(const QtModelConfig* cfg, const QtPrecisionMap* prec, cons
 
 void qt_session_destroy(qt_session* s) { delete s; }
 
+// In-process worker group (the reference's WorkerGroup, src/comms.cpp:19-38):
+// W sessions, one per host thread, on one device or several, whose collectives
+// are copy-engine pulls between their arenas (transport.cuh PeerTransport).
+int qt_group_create(int world, qt_group** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (world < 1 || world > 64) throw QtError(1, "qt_group_create: world must be in [1, 64]");
+        auto* g = new qt_group();
+        g->g = std::make_shared<PeerGroup>(world);
+        *out = g;
+    });
+}
+void qt_group_destroy(qt_group* g) { delete g; }
+
+int qt_session_create_in_group(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan,
+                               const QtAdamW* hyper, uint64_t seed, qt_group* group, int rank, int device,
+                               qt_session** out) {
+    *out = nullptr;
+    return guard([&] {
+        if (!group) throw QtError(1, "qt_session_create_in_group: null group");
+        auto* h = new qt_session();
+        try {
+            h->s = std::make_unique<Session>(*cfg, *prec, *plan, *hyper, seed, rank, group->g->world, nullptr, device,
+                                             group->g);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+// which transport a session's collectives use: "none" (world 1), "nccl", "peer-copy"
+const char* qt_session_transport(qt_session* s) { return s->s->tr ? s->s->tr->kind() : "none"; }
+
 void* qt_session_stream(qt_session* s) { return (void*)s->s->st; }
 size_t qt_session_bytes(qt_session* s) { return s->s->arena_bytes; }
 
@@ -1343,10 +1426,18 @@ static void download_bf16(Session& s, const uint16_t* src, int64_t n, float* hos
     QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
 }
 
+// With shard_weights each rank keeps only its ZeRO-1 slice of a block weight
+// current: the download gathers the owners' slices (peer group: direct reads of
+// the idle peers' arenas; NCCL: a collective every rank must enter).
 int qt_param_download(qt_session* h, int i, float* host) {
     return guard([&] {
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
+        if (s.shard_weights() && s.is_block_weight(i)) {
+            s.coll([&] { s.tr->gather_idle(s.params + t.off, (size_t)t.pw * 2, s.recvbuf, s.st); });
+            download_bf16(s, s.recvbuf, t.numel, host);
+            return;
+        }
         download_bf16(s, s.params + t.off, t.numel, host);
     });
 }
@@ -1363,12 +1454,16 @@ int qt_grad_download(qt_session* h, int i, float* host) {
 int qt_moments_download(qt_session* h, int i, float* m, float* v) {
     return guard([&] {
         Session& s = *h->s;
-        if (s.plan.bf16_moments) throw QtError(1, "bf16 moments: not supported by this accessor");
         const ParamT& t = s.P.at(i);
         std::vector<SegH> segs(s.nsegs);
         QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDeviceToHost));
         const SegH& sg = segs[i];
         const int64_t off = s.world > 1 ? sg.off : t.off;
+        if (s.plan.bf16_moments) {  // bf16-SR moments, widened to f32 (exact)
+            download_bf16(s, s.m16 + off, sg.n, m);
+            download_bf16(s, s.v16 + off, sg.n, v);
+            return;
+        }
         QT_CHECK_CUDA(cudaMemcpy(m, s.m32 + off, sg.n * 4, cudaMemcpyDeviceToHost));
         QT_CHECK_CUDA(cudaMemcpy(v, s.v32 + off, sg.n * 4, cudaMemcpyDeviceToHost));
     });
@@ -1443,9 +1538,23 @@ int qt_grad_norm(qt_session* h, double* norm_host) {
 int qt_adamw_step(qt_session* h, float grad_scale) {
     return guard([&] {
         Session& s = *h->s;
+        // g * inf (or NaN) is non-finite for every element: the reference throws on the
+        // first tensor it visits (src/optim.cpp:46-47) before changing anything
+        if (!std::isfinite(grad_scale)) throw QtError(3, "adamw_step: non-finite gradient in " + s.P[0].name);
         set_scale_kernel<<<1, 1, 0, s.st>>>(s.gscale_dev, grad_scale);
+        // gate the whole update on finite gradients (the reference throws on the first
+        // non-finite one, src/optim.cpp:47): one norm pass, then AdamW skips if *err != 0
+        s.grad_sumsq();
+        gate_kernel<<<1, 1, 0, s.st>>>(s.ssq_dev, s.err_dev);
+        QT_CHECK_CUDA(cudaGetLastError());
+        s.pre_step_count = s.step_count;
         s.adamw(s.gscale_dev);
-        s.check_errors(false);
+        try {
+            s.check_errors(false);
+        } catch (...) {
+            s.on_gated_step();
+            throw;
+        }
     });
 }
 
@@ -1455,8 +1564,15 @@ int qt_train_step(qt_session* h, const int32_t* tokens_dev, int64_t tokens_per_m
     return guard([&] {
         Session& s = *h->s;
         s.train_step(tokens_dev, tokens_per_mb, batch, step, max_grad_norm);
-        if (loss_host || norm_host) {
+        // always checked: a gated step (bad token, non-finite activation or gradient)
+        // left params and moments untouched; report it before the caller moves on
+        try {
             s.check_errors(true);
+        } catch (...) {
+            s.on_gated_step();
+            throw;
+        }
+        if (loss_host || norm_host) {
             std::vector<float> l(s.plan.ga_steps);
             double nrm = 0;
             QT_CHECK_CUDA(cudaMemcpyAsync(l.data(), s.loss_dev + 1, 4 * l.size(), cudaMemcpyDeviceToHost, s.st));
@@ -1585,6 +1701,13 @@ int qt_shard_layout(int64_t numel, int workers, int64_t* padded, int64_t* per_wo
 }
 
 uint64_t qt_fnv1a64(const char* s) { return fnv1a64(s); }
+
+// the session's RoPE table (T x hd/2 {cos, sin} float pairs) into host memory
+int qt_rope_table(int T, int hd, float* host_out) {
+    if (T < 1 || hd < 2 || (hd & 1) || !host_out) return 1;
+    rope_table_host(T, hd, reinterpret_cast<float2*>(host_out));
+    return 0;
+}
 
 // one shard of reduce_scatter_copy / reduce_scatter_oracle (src/comms.cpp:185-254):
 // srcs = W device pointers (bf16 chunks of this shard, indexed by source worker)

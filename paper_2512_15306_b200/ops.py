@@ -76,6 +76,25 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
          ce: tuple | None = None) -> torch.Tensor:
     """D[m,n] = sum_k A[m,k] B[n,k].  A stored [M][K] (a_mn=False) or [K][M]
     (a_mn=True); likewise B.  uint8 operands are FP8 codes, bf16 operands BF16."""
+    g, out, ws = _gemm_desc(a, b, M=M, N=N, K=K, a_mn=a_mn, b_mn=b_mn, a_fmt=a_fmt, b_fmt=b_fmt, a_scale=a_scale,
+                            b_scale=b_scale, epi=epi, out=out, res=res, sr=sr, bn=bn, a2=a2, split_k=split_k,
+                            amax=amax, ce=ce)
+    _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
+    return out
+
+
+def gemm_plan(a: torch.Tensor, b: torch.Tensor, **kw) -> dict:
+    """The instantiation qtk_gemm would launch for the same arguments as gemm()
+    (qtk_gemm_plan shares qtk_gemm's decision): cta_group, BN, split-K factor,
+    grid and output tiles per CTA of the persistent loop."""
+    g, _, _ = _gemm_desc(a, b, **kw)
+    o = [C.c_int() for _ in range(5)]
+    _lib.check(_lib.lib().qtk_gemm_plan(C.byref(g), *[C.byref(x) for x in o]), "qtk_gemm_plan")
+    return dict(zip(("cg", "bn", "splits", "grid", "tiles_per_cta"), (x.value for x in o)))
+
+
+def _gemm_desc(a, b, *, M, N, K, a_mn=False, b_mn=False, a_fmt=E4M3, b_fmt=E4M3, a_scale=None, b_scale=None,
+               epi=EPI_BF16, out=None, res=None, sr=(0, 0, 0), bn=0, a2=None, split_k=1, amax=None, ce=None):
     _need_cuda(a, b)
     kind = 0 if a.dtype == torch.uint8 else 1
     if out is None:
@@ -104,8 +123,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, *, M: int, N: int, K: int, a_mn: bool
     g.amax = _p(amax)
     if ce is not None:  # (targets, stats, tgt_logit): softmax statistics in the logits epilogue
         g.ce_targets, g.ce_stats, g.ce_tgt_logit = _p(ce[0]), _p(ce[1]), _p(ce[2])
-    _lib.check(_lib.lib().qtk_gemm(C.byref(g), _s()), "qtk_gemm")
-    return out
+    return g, out, ws
 
 
 def ce_softmax(logits: torch.Tensor, targets: torch.Tensor, inv_n: float, with_grads: bool = True):

@@ -160,6 +160,12 @@ _SIGS = {
     "qt_profile_read": (_ci, [_vp, _ci, _vp, _vp, _vp]),
     "qt_shard_layout": (_ci, [_i64, _ci, C.POINTER(_i64), C.POINTER(_i64)]),
     "qt_fnv1a64": (_u64, [C.c_char_p]),
+    "qt_rope_table": (_ci, [_ci, _ci, _vp]),
+    "qt_group_create": (_ci, [_ci, C.POINTER(_vp)]),
+    "qt_group_destroy": (None, [_vp]),
+    "qt_session_create_in_group": (_ci, [C.POINTER(_Cfg), C.POINTER(_Prec), C.POINTER(_Plan), C.POINTER(_Hyper),
+                                         _u64, _vp, _ci, _ci, C.POINTER(_vp)]),
+    "qt_session_transport": (C.c_char_p, [_vp]),
     "qt_count_step_kernels": (_ci, [_vp, _vp, _i64, _i64, C.POINTER(_i64), C.POINTER(_i64)]),
 }
 _bound = False
@@ -210,8 +216,59 @@ def shard_layout(numel: int, workers: int) -> tuple[int, int]:
     return p.value, w.value
 
 
+def rope_table(T: int, hd: int) -> np.ndarray:
+    """The session's RoPE table: (T, hd/2, 2) float32 {cos, sin}."""
+    out = np.empty((T, hd // 2, 2), np.float32)
+    _chk(lib().qt_rope_table(T, hd, out.ctypes.data))
+    return out
+
+
 def fnv1a64(s: str) -> int:
     return lib().qt_fnv1a64(s.encode())
+
+
+class WorkerGroup:
+    """In-process worker group (qtrain::WorkerGroup, include/qtrain/comms.hpp:51-78):
+    `world` sessions driven by one host thread each, whose collectives are
+    copy-engine pulls between the sessions' device arenas (qt_group_create)."""
+
+    def __init__(self, world: int):
+        out = _vp()
+        _chk(lib().qt_group_create(world, C.byref(out)))
+        self.h, self.world = out, world
+
+    def run(self, fn, *args_per_rank):
+        """WorkerGroup::run (src/comms.cpp:19-36): fn(rank, *args) on one thread per
+        rank; returns the per-rank results, re-raises the first exception."""
+        import threading
+        res, errs = [None] * self.world, [None] * self.world
+
+        def body(r):
+            try:
+                res[r] = fn(r, *[a[r] for a in args_per_rank])
+            except BaseException as e:  # noqa: BLE001 - rethrown below, like the reference
+                errs[r] = e
+
+        ts = [threading.Thread(target=body, args=(r,)) for r in range(self.world)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        for e in errs:
+            if e is not None:
+                raise e
+        return res
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().qt_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class Session:
@@ -219,7 +276,7 @@ class Session:
 
     def __init__(self, cfg: ModelConfig, prec: PrecisionMap | None = None, plan: RunPlan | None = None,
                  hyper: AdamWHyper | None = None, seed: int = 0, rank: int = 0, world: int = 1,
-                 nccl_id: bytes | None = None, device: int = 0):
+                 nccl_id: bytes | None = None, device: int = 0, group: WorkerGroup | None = None):
         self.cfg, self.prec = cfg, prec or PrecisionMap()
         self.plan, self.hyper = plan or RunPlan(), hyper or AdamWHyper()
         self.seed, self.rank, self.world = seed, rank, world
@@ -232,9 +289,15 @@ class Session:
         h = _Hyper(self.hyper.lr, self.hyper.beta1, self.hyper.beta2, self.hyper.eps, self.hyper.weight_decay,
                    self.hyper.max_grad_norm)
         out = _vp()
-        idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        _chk(lib().qt_session_create(C.byref(c), C.byref(p), C.byref(pl), C.byref(h), seed, rank, world, idb,
-                                     device, C.byref(out)))
+        if group is not None:
+            self.world = world = group.world
+            self._group = group  # the group outlives its sessions
+            _chk(lib().qt_session_create_in_group(C.byref(c), C.byref(p), C.byref(pl), C.byref(h), seed, group.h,
+                                                  rank, device, C.byref(out)))
+        else:
+            idb = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+            _chk(lib().qt_session_create(C.byref(c), C.byref(p), C.byref(pl), C.byref(h), seed, rank, world, idb,
+                                         device, C.byref(out)))
         self.h = out
         n = lib().qt_num_params(self.h)
         self.names, self.numel = [], []
@@ -258,6 +321,10 @@ class Session:
     @property
     def stream(self) -> int:
         return lib().qt_session_stream(self.h)
+
+    @property
+    def transport(self) -> str:
+        return lib().qt_session_transport(self.h).decode()
 
     @property
     def device_bytes(self) -> int:
@@ -287,10 +354,15 @@ class Session:
         return out
 
     def moments(self, name: str):
+        """AdamW moments; with world > 1 this rank's ZeRO-1 slice [rank*pw, (rank+1)*pw)."""
         i = self._i(name)
         n = self.numel[i]
         m, v = np.empty(n, np.float32), np.empty(n, np.float32)
         _chk(lib().qt_moments_download(self.h, i, m.ctypes.data, v.ctypes.data))
+        if self.world > 1:
+            _, pw = shard_layout(n, self.world)
+            k = max(0, min(pw, n - self.rank * pw))
+            return m[:k], v[:k]
         return m, v
 
     def set_moments(self, name: str, m, v, step_count: int) -> None:
