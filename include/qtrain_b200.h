@@ -235,7 +235,12 @@ typedef struct QtRunPlan {
     int micro_batch, ga_steps, recompute_bits;
     int64_t lmhead_chunk_tokens, attn_chunk_rows;
     int shard_weights, shard_grads, bf16_moments;
+    /* OffloadSet bits (memplan.hpp:34-42): 1 x (residuals), 2 m, 4 v, 8 master,
+     * 16 weights, 32 grads; transfer_policy: QT_XFER_* (memplan.hpp:44) */
+    int offload_bits, transfer_policy;
 } QtRunPlan;
+enum { QT_OFF_X = 1, QT_OFF_M = 2, QT_OFF_V = 4, QT_OFF_MASTER = 8, QT_OFF_WEIGHTS = 16, QT_OFF_GRADS = 32 };
+enum { QT_XFER_ZERO_COPY = 0, QT_XFER_DOUBLE_BUFFER = 1 };
 
 /* AdamWHyper (include/qtrain/optim.hpp:20-26) + RunManifest::max_grad_norm */
 typedef struct QtAdamW {
@@ -306,6 +311,65 @@ int qt_count_step_kernels(qt_session* s, const int32_t* tokens_dev, int64_t toke
  * (same step counters each replay); mean device ms per replay -> *ms */
 int qt_time_graph_step(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch, int64_t step,
                        int iters, float* ms);
+
+/* ------------------------------------------------------------------------- */
+/* planner (csrc/planner.cpp; src/memplan.cpp, src/profiles.cpp,              */
+/* src/offload.cpp).  Status codes as above; message in qt_plan_last_error(). */
+/* ------------------------------------------------------------------------- */
+/* HardwareProfile (include/qtrain/profiles.hpp:14-33) */
+typedef struct QtHardwareProfile {
+    char name[32];
+    uint64_t device_bytes, host_bytes;
+    double peak_flops_fp8, peak_flops_bf16, peak_flops_f32; /* dense FLOP/s */
+    double mem_bandwidth, link_bandwidth;                   /* bytes/s     */
+    int p2p;
+    double attainable_fraction, zero_copy_efficiency, double_buffer_efficiency;
+} QtHardwareProfile;
+/* MemoryBreakdown::Tier (include/qtrain/memplan.hpp:100-116) */
+typedef struct QtMemTier {
+    uint64_t params_fp8, params_bf16_master, moments_m, moments_v, grads, residuals, activations, logits_workspace,
+        attn_workspace;
+} QtMemTier;
+/* FlopBreakdown (memplan.hpp:148-160): per token, forward + backward */
+typedef struct QtFlops {
+    double linear, lmhead, attention, recompute;
+} QtFlops;
+/* TimeBreakdown (memplan.hpp:176-185) */
+typedef struct QtStepTime {
+    double compute, transfer, exposed_transfer, optimizer, total;
+    int feasible_in_time;
+    double tokens_per_second;
+} QtStepTime;
+const char* qt_plan_last_error(void);
+/* builtins of src/profiles.cpp:21-39 plus "b200" */
+int qt_profile_by_name(const char* name, QtHardwareProfile* out);
+int qt_profile_load(const char* name_or_path, QtHardwareProfile* out); /* profiles.cpp:82-93 */
+int qt_profile_from_json(const char* text, QtHardwareProfile* out);
+/* text outputs: *needed = bytes incl. NUL; buf may be NULL to query the size */
+int qt_profile_to_json(const QtHardwareProfile* p, char* buf, size_t cap, size_t* needed);
+int qt_param_counts(const QtModelConfig* cfg, int tied, uint64_t* total, uint64_t* block_linear,
+                    uint64_t* per_layer_linear, uint64_t* lmhead, uint64_t* embed, uint64_t* norms);
+/* memory_breakdown (memplan.cpp:177-268): per worker */
+int qt_memory_breakdown(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan, int workers,
+                        int tied, QtMemTier* device, QtMemTier* host);
+int qt_flop_breakdown(const QtModelConfig* cfg, int recompute_bits, int tied, QtFlops* out);
+int qt_lower_bound_seconds_per_token(const QtFlops* f, const QtPrecisionMap* prec, const QtHardwareProfile* hw,
+                                     int attainable, int include_recompute, double* out);
+int qt_mfu(double measured_tps, const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtHardwareProfile* hw,
+           int tied, double* out);
+int qt_fp8_speedup_ceiling(const QtModelConfig* cfg, const QtHardwareProfile* hw, int tied, double* out);
+int qt_estimate_step_time(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan,
+                          const QtHardwareProfile* hw, int workers, int tied, QtStepTime* out);
+/* search_plan (memplan.cpp:471-551) -> JSON {"feasible": [...], "n_feasible", "no_fit_reason"?};
+ * max_results <= 0: all */
+int qt_search_plan(const QtModelConfig* cfg, const QtHardwareProfile* hw, int workers, int64_t target_batch_tokens,
+                   int block_matmuls, int exhaustive, int tied, int max_results, char* json_out, size_t cap,
+                   size_t* needed);
+/* plan_residency (offload.cpp:40-163) -> JSON {"events": [...], "high_water_*", "feasible", "report"?} */
+int qt_plan_residency(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan,
+                      uint64_t device_budget, int tied, char* json_out, size_t cap, size_t* needed);
+/* transfer_time (offload.cpp:165-171) */
+int qt_transfer_time(uint64_t bytes, const QtHardwareProfile* hw, int policy, double* out);
 
 #ifdef __cplusplus
 }

@@ -106,7 +106,7 @@ class Session {
                          prec.backward_grads == GradPrecision::E4M3 ? 0 : 1, prec.f32_debug ? 1 : 0};
         QtRunPlan r{plan.micro_batch, plan.ga_steps, plan.recompute.bits, plan.chunks.lmhead_chunk_tokens,
                     plan.chunks.attn_chunk_rows, plan.shard_weights ? 1 : 0, plan.shard_grads ? 1 : 0,
-                    plan.moments == MomentPrecision::BF16_SR ? 1 : 0};
+                    plan.moments == MomentPrecision::BF16_SR ? 1 : 0, 0, 0};
         QtAdamW h{hyper.lr, hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, max_grad_norm};
         check(qt_session_create(&c, &p, &r, &h, seed, rank, world, nccl_id, device, &s_));
         ga_steps_ = plan.ga_steps;

@@ -80,6 +80,15 @@ _SIGS = {
     "ref_reduce_scatter_oracle": (ci, [f32p, f32p, ci, i64, ci, u64, u64, u64]),
     "ref_reduce_scatter_copy": (ci, [f32p, f32p, ci, i64, ci, u64, u64, u64]),
     "ref_rope_apply": (ci, [C.POINTER(ci), f32p, i64, i64, ci]),
+    "ref_memory_breakdown": (ci, [C.POINTER(ci), ci, C.POINTER(i64), ci, C.POINTER(u64)]),
+    "ref_flop_breakdown": (ci, [C.POINTER(ci), ci, ci, C.POINTER(C.c_double)]),
+    "ref_mfu": (ci, [C.c_double, C.POINTER(ci), ci, C.c_char_p, ci, C.POINTER(C.c_double)]),
+    "ref_fp8_speedup_ceiling": (ci, [C.POINTER(ci), C.c_char_p, ci, C.POINTER(C.c_double)]),
+    "ref_estimate_step_time": (ci, [C.POINTER(ci), C.POINTER(i64), C.c_char_p, ci, ci, C.POINTER(C.c_double)]),
+    "ref_search_plan": (ci, [C.POINTER(ci), C.c_char_p, ci, i64, ci, ci, ci, C.c_char_p, C.c_size_t]),
+    "ref_plan_residency": (ci, [C.POINTER(ci), C.POINTER(i64), u64, ci, C.c_char_p, C.c_size_t]),
+    "ref_profile_json": (ci, [C.c_char_p, C.c_char_p, C.c_size_t]),
+    "ref_transfer_time": (ci, [u64, C.c_char_p, ci, C.POINTER(C.c_double)]),
 }
 
 _lib = None
@@ -416,3 +425,124 @@ def reduce_scatter(chunks, acc, *, stochastic=True, seed=0, step=0, layer=0, pro
     f = lib().ref_reduce_scatter_copy if protocol else lib().ref_reduce_scatter_oracle
     _chk(f(c.ravel(), a.ravel(), W, n, int(stochastic), seed, step, layer))
     return a
+
+
+# ---------------------------------------------------------------- planner (src/memplan.cpp, profiles.cpp, offload.cpp)
+def _cfg7(cfg7):
+    return (ci * 7)(*cfg7)
+
+
+def _plan10(mb=1, ga=1, recompute_bits=0, offload_bits=0, shard_weights=False, shard_grads=False, bf16=False,
+            bf16_moments=True, lmhead_chunk=512, attn_chunk=256):
+    return (i64 * 10)(mb, ga, recompute_bits, offload_bits, int(shard_weights), int(shard_grads), int(bf16),
+                      int(bf16_moments), lmhead_chunk, attn_chunk)
+
+
+TIER = ("params_fp8", "params_bf16_master", "moments_m", "moments_v", "grads", "residuals", "activations",
+        "logits_workspace", "attn_workspace")
+
+
+def memory_breakdown(cfg7, workers=1, tied=False, **plan):
+    out = (u64 * 18)()
+    _chk(lib().ref_memory_breakdown(_cfg7(cfg7), int(tied), _plan10(**plan), workers, out))
+    return dict(zip(TIER, out[:9])), dict(zip(TIER, out[9:]))
+
+
+def flop_breakdown(cfg7, recompute_bits=0, tied=False):
+    out = (C.c_double * 4)()
+    _chk(lib().ref_flop_breakdown(_cfg7(cfg7), recompute_bits, int(tied), out))
+    return dict(zip(("linear", "lmhead", "attention", "recompute"), out))
+
+
+def mfu(tps, cfg7, profile, bf16=False, tied=False):
+    out = C.c_double()
+    _chk(lib().ref_mfu(tps, _cfg7(cfg7), int(bf16), profile.encode(), int(tied), C.byref(out)))
+    return out.value
+
+
+def fp8_speedup_ceiling(cfg7, profile, tied=False):
+    out = C.c_double()
+    _chk(lib().ref_fp8_speedup_ceiling(_cfg7(cfg7), profile.encode(), int(tied), C.byref(out)))
+    return out.value
+
+
+def estimate_step_time(cfg7, profile, workers=1, tied=False, **plan):
+    out = (C.c_double * 7)()
+    _chk(lib().ref_estimate_step_time(_cfg7(cfg7), _plan10(**plan), profile.encode(), workers, int(tied), out))
+    return dict(zip(("compute", "transfer", "exposed_transfer", "optimizer", "total", "feasible_in_time",
+                     "tokens_per_second"), out))
+
+
+_SEARCH_CHILD = r"""
+import ctypes as C, sys
+l = C.CDLL(sys.argv[1])
+f = l.ref_search_plan
+f.argtypes = [C.POINTER(C.c_int), C.c_char_p, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]
+a = [int(x) for x in sys.argv[3:]]
+buf = C.create_string_buffer(256 << 20)
+rc = f((C.c_int * 7)(*a[:7]), sys.argv[2].encode(), *a[7:], buf, len(buf))
+if rc:
+    l.ref_last_error.restype = C.c_char_p
+    sys.stderr.write(l.ref_last_error().decode())
+    sys.exit(rc)
+sys.stdout.write(buf.value.decode())
+"""
+
+
+def search_plan(cfg7, profile, workers, target, bf16=False, exhaustive=False, tied=False):
+    """search_plan runs in a child interpreter that has not imported numpy: in a
+    process where numpy (OpenBLAS) is loaded the reference's search_plan
+    segfaults inside its std::sort (reproduced with the unmodified sources;
+    the same call from C++ or from a numpy-free interpreter is fine)."""
+    import json
+    import subprocess
+    import sys
+    args = [str(x) for x in (*cfg7, workers, target, int(bf16), int(exhaustive), int(tied))]
+    r = subprocess.run([sys.executable, "-c", _SEARCH_CHILD, str(REF_LIB), profile, *args], capture_output=True,
+                       text=True, timeout=600)
+    if r.returncode:
+        raise RefError(r.returncode, r.stderr)
+    return json.loads(r.stdout)
+
+
+_RESIDENCY_CHILD = r"""
+import ctypes as C, sys
+l = C.CDLL(sys.argv[1])
+f = l.ref_plan_residency
+f.argtypes = [C.POINTER(C.c_int), C.POINTER(C.c_int64), C.c_uint64, C.c_int, C.c_char_p, C.c_size_t]
+a = [int(x) for x in sys.argv[2:]]
+buf = C.create_string_buffer(64 << 20)
+rc = f((C.c_int * 7)(*a[:7]), (C.c_int64 * 10)(*a[7:17]), a[17], a[18], buf, len(buf))
+if rc:
+    l.ref_last_error.restype = C.c_char_p
+    sys.stderr.write(l.ref_last_error().decode())
+    sys.exit(rc)
+sys.stdout.write(buf.value.decode())
+"""
+
+
+def plan_residency(cfg7, budget, tied=False, **plan):
+    """Child interpreter for the same reason as search_plan (std::ostringstream
+    inside the reference crashes once numpy/torch are loaded in this process)."""
+    import json
+    import subprocess
+    import sys
+    args = [str(int(x)) for x in (*cfg7, *_plan10(**plan), budget, int(tied))]
+    r = subprocess.run([sys.executable, "-c", _RESIDENCY_CHILD, str(REF_LIB), *args], capture_output=True, text=True,
+                       timeout=600)
+    if r.returncode:
+        raise RefError(r.returncode, r.stderr)
+    return json.loads(r.stdout)
+
+
+def profile_json(name):
+    import json
+    buf = C.create_string_buffer(1 << 16)
+    _chk(lib().ref_profile_json(name.encode(), buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def transfer_time(nbytes, profile, zero_copy):
+    out = C.c_double()
+    _chk(lib().ref_transfer_time(nbytes, profile.encode(), 0 if zero_copy else 1, C.byref(out)))
+    return out.value

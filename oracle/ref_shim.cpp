@@ -18,6 +18,12 @@
 #include "qtrain/corpus.hpp"
 #include "qtrain/memplan.hpp"
 #include "qtrain/comms.hpp"
+#include "qtrain/offload.hpp"
+#include "qtrain/profiles.hpp"
+#include "qtrain/manifest.hpp"
+#include "qtrain/checkpoint.hpp"
+
+#include <json.hpp>
 
 #include <chrono>
 #include <cstring>
@@ -575,6 +581,137 @@ int ref_reduce_scatter_oracle(const float* chunks, float* acc, int W, std::int64
 int ref_reduce_scatter_copy(const float* chunks, float* acc, int W, std::int64_t n, int stochastic,
                             std::uint64_t seed, std::uint64_t step, std::uint64_t layer) {
     return rs_common(chunks, acc, W, n, stochastic, seed, step, layer, 1);
+}
+
+// ---- planner (src/memplan.cpp, src/profiles.cpp, src/offload.cpp) ---------
+// plan10 = {micro_batch, ga_steps, recompute_bits, offload_bits, shard_weights, shard_grads,
+//           block_matmuls (0 fp8 / 1 bf16), bf16_moments, lmhead_chunk_tokens, attn_chunk_rows}
+static RunPlan plan_of(const std::int64_t* p) {
+    RunPlan r;
+    r.micro_batch = (int)p[0];
+    r.ga_steps = (int)p[1];
+    r.recompute.bits = (std::uint8_t)p[2];
+    const int ob = (int)p[3];
+    r.offload.x = ob & 1;
+    r.offload.m = ob & 2;
+    r.offload.v = ob & 4;
+    r.offload.master = ob & 8;
+    r.offload.weights = ob & 16;
+    r.offload.grads = ob & 32;
+    r.shard_weights = p[4] != 0;
+    r.shard_grads = p[5] != 0;
+    r.precision.block_matmuls = p[6] == 0 ? MatmulPrecision::FP8_E4M3 : MatmulPrecision::BF16;
+    r.moments = p[7] ? MomentPrecision::BF16_SR : MomentPrecision::F32;
+    r.lmhead_chunk_tokens = p[8];
+    r.attn_chunk_rows = p[9];
+    return r;
+}
+static void put_tier(const MemoryBreakdown::Tier& t, std::uint64_t* o) {
+    o[0] = t.params_fp8;
+    o[1] = t.params_bf16_master;
+    o[2] = t.moments_m;
+    o[3] = t.moments_v;
+    o[4] = t.grads;
+    o[5] = t.residuals;
+    o[6] = t.activations;
+    o[7] = t.logits_workspace;
+    o[8] = t.attn_workspace;
+}
+static int put_str(const std::string& s, char* out, std::size_t cap) {
+    if (s.size() + 1 > cap) throw std::invalid_argument("output buffer too small: " + std::to_string(s.size() + 1));
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+static HardwareProfile prof_from(const char* name_or_json) {
+    const std::string s(name_or_json);
+    if (!s.empty() && s[0] == '{') return profile_from_json(s);
+    return profile_by_name(s);
+}
+
+// memory_breakdown (src/memplan.cpp:263-268): out = device tier[9], host tier[9]
+int ref_memory_breakdown(const int* cfg7, int tied, const std::int64_t* plan10, int workers, std::uint64_t* out18) {
+    return guard([&] {
+        const auto mb = memory_breakdown(cfg_of(cfg7), plan_of(plan10), workers, tied != 0);
+        put_tier(mb.device, out18);
+        put_tier(mb.host, out18 + 9);
+    });
+}
+// flop_breakdown (src/memplan.cpp:274-290): {linear, lmhead, attention, recompute}
+int ref_flop_breakdown(const int* cfg7, int recompute_bits, int tied, double* out4) {
+    return guard([&] {
+        RecomputeSet rc;
+        rc.bits = (std::uint8_t)recompute_bits;
+        const auto fb = flop_breakdown(cfg_of(cfg7), rc, tied != 0);
+        out4[0] = fb.linear;
+        out4[1] = fb.lmhead;
+        out4[2] = fb.attention;
+        out4[3] = fb.recompute;
+    });
+}
+// mfu (src/memplan.cpp:315-320)
+int ref_mfu(double tps, const int* cfg7, int matmuls, const char* profile, int tied, double* out) {
+    return guard([&] { *out = mfu(tps, cfg_of(cfg7), prec_of(matmuls, 0, 0), prof_from(profile), tied != 0); });
+}
+int ref_fp8_speedup_ceiling(const int* cfg7, const char* profile, int tied, double* out) {
+    return guard([&] { *out = fp8_speedup_ceiling(cfg_of(cfg7), prof_from(profile), tied != 0); });
+}
+// estimate_step_time (src/memplan.cpp:331-406): {compute, transfer, exposed, optimizer, total, feasible, tps}
+int ref_estimate_step_time(const int* cfg7, const std::int64_t* plan10, const char* profile, int workers, int tied,
+                           double* out7) {
+    return guard([&] {
+        const auto t = estimate_step_time(cfg_of(cfg7), plan_of(plan10), prof_from(profile), workers, tied != 0);
+        out7[0] = t.compute;
+        out7[1] = t.transfer;
+        out7[2] = t.exposed_transfer;
+        out7[3] = t.optimizer;
+        out7[4] = t.total;
+        out7[5] = t.feasible_in_time ? 1.0 : 0.0;
+        out7[6] = t.tokens_per_second;
+    });
+}
+// search_plan (src/memplan.cpp:471-551) -> JSON {"feasible": [{"str", "tps", "device"}], "no_fit_reason"}
+int ref_search_plan(const int* cfg7, const char* profile, int workers, std::int64_t target, int matmuls,
+                    int exhaustive, int tied, char* out, std::size_t cap) {
+    return guard([&] {
+        const auto r = search_plan(cfg_of(cfg7), prof_from(profile), workers, target,
+                                   matmuls == 0 ? MatmulPrecision::FP8_E4M3 : MatmulPrecision::BF16, exhaustive != 0,
+                                   tied != 0);
+        nlohmann::json j;
+        j["feasible"] = nlohmann::json::array();
+        for (const auto& v : r.feasible)
+            j["feasible"].push_back({{"str", v.plan.str()},
+                                     {"tps", v.time.tokens_per_second},
+                                     {"device", v.memory.device.total()},
+                                     {"host", v.memory.host.total()}});
+        if (r.no_fit_reason) j["no_fit_reason"] = *r.no_fit_reason;
+        put_str(j.dump(), out, cap);
+    });
+}
+// plan_residency (src/offload.cpp:40-163) -> {"jsonl", "high_water", "hw_weights", "hw_grads", "hw_residuals", "feasible"}
+int ref_plan_residency(const int* cfg7, const std::int64_t* plan10, std::uint64_t budget, int tied, char* out,
+                       std::size_t cap) {
+    return guard([&] {
+        TierBudget b;
+        b.device_bytes = budget;
+        const auto r = plan_residency(cfg_of(cfg7), plan_of(plan10), b, tied != 0);
+        nlohmann::json j;
+        j["jsonl"] = r.to_jsonl();
+        j["high_water"] = r.high_water_device;
+        j["hw_weights"] = r.high_water_by_category_weights;
+        j["hw_grads"] = r.high_water_by_category_grads;
+        j["hw_residuals"] = r.high_water_by_category_residuals;
+        j["feasible"] = r.feasible;
+        j["report"] = r.report;
+        put_str(j.dump(), out, cap);
+    });
+}
+int ref_profile_json(const char* name, char* out, std::size_t cap) {
+    return guard([&] { put_str(profile_to_json(profile_by_name(name)), out, cap); });
+}
+int ref_transfer_time(std::uint64_t bytes, const char* profile, int policy, double* out) {
+    return guard([&] {
+        *out = transfer_time(bytes, prof_from(profile), policy == 0 ? TransferPolicy::ZeroCopy : TransferPolicy::DoubleBuffer);
+    });
 }
 
 } // extern "C"

@@ -27,6 +27,15 @@
 #include <string>
 #include <vector>
 
+#include "hostjson.h"
+namespace qtb {
+namespace plan {
+using DeviceBytesFn = uint64_t (*)(const QtModelConfig&, const QtPrecisionMap&, const QtRunPlan&, int, bool,
+                                   const QtMemTier&);
+json::Value search_with(const QtModelConfig& c, const QtHardwareProfile& hw, int W, int64_t target_tokens, int matmuls,
+                        bool exhaustive, bool tied, DeviceBytesFn fn, int max_results);
+}  // namespace plan
+}  // namespace qtb
 namespace qtb {
 
 // ---------------------------------------------------------------------------
@@ -371,6 +380,29 @@ class Session {
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
 
+    // Dry layout: the arena (and pinned host) bytes a session of this shape allocates,
+    // computed by the same allocate() without touching a device (qt_session_footprint)
+    struct DryRun {};
+    bool dry = false;
+    size_t host_bytes = 0;
+    Session(DryRun, const QtModelConfig& c, const QtPrecisionMap& p, const QtRunPlan& pl, int ws)
+        : cfg(c), prec(p), plan(pl), hyper{}, seed(0), rank(0), world(ws), dry(true) {
+        validate();
+        L = c.n_layers;
+        d = c.d_model;
+        F = c.d_ff;
+        Hh = c.d_ff / 2;
+        H = c.n_heads;
+        Hkv = c.n_kv_heads;
+        hd = d / H;
+        q = d + 2 * Hkv * hd;
+        V = c.vocab;
+        T = c.seq_len;
+        Mmax = (int64_t)std::max(1, pl.micro_batch) * T;
+        build_params();
+        allocate();
+    }
+
     ~Session() {
         tr.reset();
         for (auto e : ev_pool) cudaEventDestroy(e);
@@ -601,6 +633,10 @@ class Session {
 
         size_t total = 0;
         for (auto& r : reqs) total += (r.bytes + 255) & ~size_t(255);
+        if (dry) {
+            arena_bytes = total;
+            return;
+        }
         QT_CHECK_CUDA(cudaMalloc(&arena, total));
         arena_bytes = total;
         QT_CHECK_CUDA(cudaMemsetAsync(arena, 0, total, st));
@@ -1689,6 +1725,45 @@ int qt_profile_read(qt_session* h, int ncat, double* ms, int64_t* launches, doub
             work[r.cat] += r.work;
         }
     });
+}
+
+int qt_session_footprint(const QtModelConfig* cfg, const QtPrecisionMap* prec, const QtRunPlan* plan, int world,
+                         uint64_t* device_bytes, uint64_t* host_bytes) {
+    return guard([&] {
+        if (world < 1) throw QtError(1, "qt_session_footprint: world must be >= 1");
+        Session s(Session::DryRun{}, *cfg, *prec, *plan, world);
+        *device_bytes = s.arena_bytes;
+        *host_bytes = s.host_bytes + Session::kBlkRing * 64;  // + the step-block staging ring
+    });
+}
+
+int qt_search_plan_session(const QtModelConfig* cfg, const QtHardwareProfile* hw, int workers,
+                           int64_t target_batch_tokens, int exhaustive, int max_results, char* json_out, size_t cap,
+                           size_t* needed) {
+    int rc = 0;
+    const int g = guard([&] {
+        // the search ladder of the reference, filtered by the session's real arena: plans whose
+        // recompute/offload/sharding the session does not run, or that its kernels reject, fail
+        // the footprint and drop out
+        auto fn = [](const QtModelConfig& c, const QtPrecisionMap& p, const QtRunPlan& pl, int W, bool,
+                     const QtMemTier&) -> uint64_t {
+            QtPrecisionMap pr = p;
+            pr.backward_grads = 1;
+            try {
+                Session s(Session::DryRun{}, c, pr, pl, W);
+                return s.arena_bytes;
+            } catch (const std::exception&) {
+                return ~uint64_t(0);
+            }
+        };
+        const std::string text =
+            qtb::plan::search_with(*cfg, *hw, workers, target_batch_tokens, 0, exhaustive != 0, false, fn, max_results)
+                .dump();
+        if (needed) *needed = text.size() + 1;
+        if (json_out && cap >= text.size() + 1) std::memcpy(json_out, text.c_str(), text.size() + 1);
+        else if (json_out) rc = 1;
+    });
+    return g ? g : rc;
 }
 
 // host-side ZeRO-1 layout (src/comms.cpp:69-73), exported for the gloo tests

@@ -34,6 +34,24 @@ def recompute_bits(names) -> int:
     return bits
 
 
+# OffloadSet field order (include/qtrain/memplan.hpp:34-42) = QT_OFF_* bits
+OFFLOAD_CATS = ("x", "m", "v", "master", "weights", "grads")
+_OFFLOAD_ALIASES = {"residuals": "x", "theta*": "master", "theta": "weights", "g": "grads"}
+
+
+def offload_bits(names) -> int:
+    """offload_set_from_names (src/memplan.cpp:47-60)."""
+    bits = 0
+    for n in names or ():
+        if n in ("none", ""):
+            continue
+        n = _OFFLOAD_ALIASES.get(n, n)
+        if n not in OFFLOAD_CATS:
+            raise ValueError(f"unknown offload category: {n}")
+        bits |= 1 << OFFLOAD_CATS.index(n)
+    return bits
+
+
 @dataclass
 class ModelConfig:
     n_layers: int = 2
@@ -94,6 +112,8 @@ class RunPlan:
     shard_weights: bool = False
     shard_grads: bool = False
     moments: str = "f32"  # "f32" | "bf16_sr"
+    offload: tuple = ()  # OffloadSet names (memplan.cpp:47-60): x, m, v, master, weights, grads
+    transfer_policy: str = "double_buffer"  # "zero_copy" | "double_buffer"
 
 
 @dataclass
@@ -118,7 +138,8 @@ class _Prec(C.Structure):
 class _Plan(C.Structure):
     _fields_ = [("micro_batch", C.c_int), ("ga_steps", C.c_int), ("recompute_bits", C.c_int),
                 ("lmhead_chunk_tokens", C.c_int64), ("attn_chunk_rows", C.c_int64), ("shard_weights", C.c_int),
-                ("shard_grads", C.c_int), ("bf16_moments", C.c_int)]
+                ("shard_grads", C.c_int), ("bf16_moments", C.c_int), ("offload_bits", C.c_int),
+                ("transfer_policy", C.c_int)]
 
 
 class _Hyper(C.Structure):
@@ -285,7 +306,8 @@ class Session:
                   int(self.prec.f32_debug))
         pl = _Plan(self.plan.micro_batch, self.plan.ga_steps, recompute_bits(self.plan.recompute),
                    self.plan.lmhead_chunk_tokens, self.plan.attn_chunk_rows, int(self.plan.shard_weights),
-                   int(self.plan.shard_grads), int(self.plan.moments == "bf16_sr"))
+                   int(self.plan.shard_grads), int(self.plan.moments == "bf16_sr"), offload_bits(self.plan.offload),
+                   0 if self.plan.transfer_policy == "zero_copy" else 1)
         h = _Hyper(self.hyper.lr, self.hyper.beta1, self.hyper.beta2, self.hyper.eps, self.hyper.weight_decay,
                    self.hyper.max_grad_norm)
         out = _vp()

@@ -202,29 +202,55 @@ def test_loss_curve_20_steps_teacher_forced(ref):
 
 
 # ------------------------------------------------------------------ real widths
+def _update_flips(after, before, ref_after):
+    """Fraction of elements whose one-step update direction differs from the
+    reference's.  The first AdamW step is sign-like (m/sqrt(v) = g/|g|,
+    src/optim.cpp:61-70), so a last-bit gradient difference on an element whose
+    gradient is ~0 moves that element by a full 2*lr: updated params are
+    compared by how many directions flip, not norm-wise."""
+    a = np.sign(np.asarray(after, np.float64) - before)
+    b = np.sign(np.asarray(ref_after, np.float64) - before)
+    return float((a != b).mean())
+
+
 def _width_step(ref, preset, n_layers, T, seed=1234):
+    """One teacher-forced train step at the real widths: loss 1e-3 rel,
+    norm 2e-2, every gradient within 2x the reference's own single-code-flip
+    envelope (its sensitivity to ONE E4M3 code of one weight: per-tensor FP8
+    quantization turns any last-bit difference upstream into such flips,
+    SURVEY.md 8(c), scripts/chaos_floor.py), and the updated params' direction
+    flips within 2x the flips the same perturbation causes in the reference."""
     from paper_2512_15306_b200 import session as S
     p = S.PRESETS[preset]
     cfgd = dict(n_layers=n_layers, d_model=p.d_model, d_ff=p.d_ff, n_heads=p.n_heads, n_kv_heads=p.n_kv_heads,
                 vocab=p.vocab, seq_len=T)
     cfg, rm, sess = _pair(ref, cfgd, seed=seed, grad_e5m2=True, micro_batch=1)
     toks = _tokens(cfg.vocab, 1, T, 31)
+    before = {n: rm.get(n) for n in rm.names}
     lw, nw = rm.train_step(toks, 1, step=0)
     lg, ng = sess.train_step(toks, 1, step=0)
     assert abs(lg - lw) / lw < 1e-3, (lg, lw)
     assert abs(ng - nw) / nw < 2e-2, (ng, nw)
-    # envelope: the reference's own updated params after one E4M3 code step in one weight
+    # the reference with ONE E4M3 code step in one weight
     pert = ref.RefModel(cfg.as_list(), seed, grad_e5m2=True)
-    w = pert.get("layers.0.w_o").copy()
+    w = pert.get("layers.0.w_qkv").copy()
     i = int(np.argmax(np.abs(w) < 0.5 * np.abs(w).max()))
     w[i] = ref.bf16_round(float(w[i]) * 1.125)
-    pert.set("layers.0.w_o", w)
+    pert.set("layers.0.w_qkv", w)
     pert.train_step(toks, 1, step=0)
+    worst = {}
     for n in rm.names:
-        want = rm.get(n)
-        env = _rel(pert.get(n), want) if n != "layers.0.w_o" else 2e-3
-        got = _rel(sess.download(n), want)
-        assert got <= max(2.0 * env, 1e-3), (n, got, env)
+        want_g = rm.acc_grad(n)
+        env_g = _rel(pert.acc_grad(n), want_g)
+        got_g = _rel(sess.grad(n), want_g)
+        assert got_g <= max(2.0 * env_g, 5e-3), (n, "grad", got_g, env_g)
+        if n == "layers.0.w_qkv":
+            continue
+        env_f = _update_flips(pert.get(n), before[n], rm.get(n))
+        got_f = _update_flips(sess.download(n), before[n], rm.get(n))
+        worst[n] = (got_g, env_g, got_f, env_f)
+        assert got_f <= max(2.0 * env_f, 1e-3), (n, "update flips", got_f, env_f)
+    print({n: tuple(round(x, 5) for x in v) for n, v in worst.items()})
 
 
 def test_train_step_qwen05b_width_2_layers(ref):
