@@ -183,6 +183,20 @@ int qtk_ce_softmax(const float* logits, int64_t ldl, int64_t rows, int V, const 
 int qtk_ce_softmax_stats(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets,
                          const float* stats, const float* tgt_logit, float inv_n, void* dlogits, void* dlogits_lo,
                          int64_t ldd, float* loss_rows, cudaStream_t s);
+/* the target-exact CE backward (DESIGN.md §2 A15): as qtk_ce_softmax_stats, but
+ * dlogits (bf16) has the target entry zeroed and dl_tgt[row] = (p_t - 1) / N
+ * (f32) holds it; no lo part */
+int qtk_ce_softmax_stats_tx(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets,
+                            const float* stats, const float* tgt_logit, float inv_n, void* dlogits, int64_t ldd,
+                            float* loss_rows, float* dl_tgt, cudaStream_t s);
+/* d_hidden = bf16(acc + dl_tgt[m] * lm_w[targets[m]])   (acc: f32 M x d, the
+ * split-K sum of bf16(dlogits) . lm_w) */
+int qtk_lm_dgrad_finish(const float* acc, int64_t M, int d, const float* dl_tgt, const int32_t* targets,
+                        const void* lm_w, void* d_hidden, cudaStream_t s);
+/* acc[v] += sum_{m: targets[m] = v} dl_tgt[m] * hidden[m], ascending m, over the
+ * segments of qtk_embed_sort(targets) (acc: f32 V x d) */
+int qtk_lm_wgrad_targets(float* acc, int d, const int32_t* sorted_pos, const int32_t* seg_tok, const int32_t* seg_off,
+                         const int* nseg, int64_t max_segs, const float* dl_tgt, const void* hidden, cudaStream_t s);
 int qtk_loss_reduce(const float* loss_rows, int64_t n, float inv_n, float* out, float* accum, cudaStream_t s);
 
 /* optimizer (src/optim.cpp:37-110).  segs: device array of per-tensor segment
@@ -277,8 +291,17 @@ int qt_param_info(qt_session* s, int i, const char** name, int64_t* numel);
 int qt_param_upload(qt_session* s, int i, const float* host);
 int qt_param_download(qt_session* s, int i, float* host);
 int qt_grad_download(qt_session* s, int i, float* host);
+/* world > 1: the cross-rank reduced f32 gradient of tensor i (all ranks' shards gathered) */
+int qt_reduced_grad_download(qt_session* s, int i, float* host);
 int qt_moments_download(qt_session* s, int i, float* m, float* v);
+/* m, v: the full tensor; each rank stores its ZeRO-1 slice (bf16-SR moments: values on the bf16 grid) */
 int qt_moments_upload(qt_session* s, int i, const float* m, const float* v, int64_t step_count);
+/* the slice [lo, lo + n) of tensor i that qt_moments_download returns on this rank */
+int qt_moments_slice(qt_session* s, int i, int64_t* lo, int64_t* n);
+int qt_step_count(qt_session* s, int64_t* out);
+/* per-micro-batch losses of the last qt_train_step on this rank (ga_steps floats) */
+int qt_step_losses(qt_session* s, float* out);
+int qt_session_rank(qt_session* s, int* rank, int* world);
 int qt_init_params(qt_session* s, uint64_t seed);                 /* init_params, model.cpp:67-86   */
 int qt_build_step_context(qt_session* s);                          /* build_step_context, :88-107    */
 int qt_forward(qt_session* s, const int32_t* tokens_dev, int64_t n_tokens, int64_t batch, int with_grads,
@@ -341,6 +364,8 @@ typedef struct QtStepTime {
     double tokens_per_second;
 } QtStepTime;
 const char* qt_plan_last_error(void);
+/* model_presets (src/memplan.cpp:98-108): toy, 0.5b, 1.5b, 3b, 7b, 14b, 32b */
+int qt_model_preset(const char* name, QtModelConfig* cfg, int* tied);
 /* builtins of src/profiles.cpp:21-39 plus "b200" */
 int qt_profile_by_name(const char* name, QtHardwareProfile* out);
 int qt_profile_load(const char* name_or_path, QtHardwareProfile* out); /* profiles.cpp:82-93 */
@@ -370,6 +395,29 @@ int qt_plan_residency(const QtModelConfig* cfg, const QtPrecisionMap* prec, cons
                       uint64_t device_budget, int tied, char* json_out, size_t cap, size_t* needed);
 /* transfer_time (offload.cpp:165-171) */
 int qt_transfer_time(uint64_t bytes, const QtHardwareProfile* hw, int policy, double* out);
+
+/* ------------------------------------------------------------------------- */
+/* trainer, corpora, checkpoints (csrc/trainer.cpp; src/trainer.cpp,          */
+/* src/manifest.cpp, src/corpus.cpp, src/checkpoint.cpp).  Errors: status as  */
+/* above, message in qt_train_last_error().                                  */
+/* ------------------------------------------------------------------------- */
+const char* qt_train_last_error(void);
+/* make_corpus (corpus.cpp:58-69): kind "perm-walk" | "uniform"; train_out n_train*(seq_len+1),
+ * val_out n_val*(seq_len+1) ids */
+int qt_make_corpus(const char* kind, int64_t vocab, int seq_len, int n_train, int n_val, uint64_t seed,
+                   int32_t* train_out, int32_t* val_out);
+/* manifest_to_json(manifest_from_json(text or path)) (manifest.cpp:45-188) */
+int qt_manifest_normalize(const char* manifest, char* json_out, size_t cap, size_t* needed);
+/* run_training_to_files (trainer.cpp:35-171) on the device: metrics CSV and the QTCKPT01
+ * checkpoint per the manifest's outputs; "resume_from": <checkpoint> continues a run;
+ * W workers = W sessions of one peer group on device w % device_count (0 = all visible).
+ * result_json: {"metrics": [...], "initial_train_loss", "final_train_loss", "final_val_loss"} */
+int qt_run_training(const char* manifest, int device_count, char* result_json, size_t cap, size_t* needed);
+/* QTCKPT01 (checkpoint.cpp:19-80) of the params (for_each_param order), optional optimizer
+ * moments ("optim.m.<name>", "optim.v.<name>", name order) and "optim.step" */
+int qt_checkpoint_save(qt_session* const* sessions, int n_sessions, const QtModelConfig* cfg, const char* path,
+                       int with_optimizer);
+int qt_checkpoint_load(qt_session* const* sessions, int n_sessions, const char* path, int64_t* step_out);
 
 #ifdef __cplusplus
 }

@@ -89,6 +89,8 @@ _SIGS = {
     "ref_plan_residency": (ci, [C.POINTER(ci), C.POINTER(i64), u64, ci, C.c_char_p, C.c_size_t]),
     "ref_profile_json": (ci, [C.c_char_p, C.c_char_p, C.c_size_t]),
     "ref_transfer_time": (ci, [u64, C.c_char_p, ci, C.POINTER(C.c_double)]),
+    "ref_manifest_normalize": (ci, [C.c_char_p, C.c_char_p, C.c_size_t]),
+    "ref_run_training": (ci, [C.c_char_p, C.c_char_p, C.c_size_t]),
 }
 
 _lib = None
@@ -546,3 +548,19 @@ def transfer_time(nbytes, profile, zero_copy):
     out = C.c_double()
     _chk(lib().ref_transfer_time(nbytes, profile.encode(), 0 if zero_copy else 1, C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------- manifest / trainer (src/manifest.cpp, trainer.cpp)
+def manifest_normalize(text: str) -> dict:
+    import json
+    buf = C.create_string_buffer(1 << 20)
+    _chk(lib().ref_manifest_normalize(text.encode(), buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+def run_training(manifest_text: str) -> str:
+    """The reference trainer (run_training_to_files): writes the manifest's metrics CSV and
+    checkpoint, returns the CSV text."""
+    buf = C.create_string_buffer(16 << 20)
+    _chk(lib().ref_run_training(manifest_text.encode(), buf, len(buf)))
+    return buf.value.decode()

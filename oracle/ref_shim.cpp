@@ -714,4 +714,16 @@ int ref_transfer_time(std::uint64_t bytes, const char* profile, int policy, doub
     });
 }
 
+// ---- manifest / trainer / checkpoint (src/manifest.cpp, src/trainer.cpp, src/checkpoint.cpp)
+int ref_manifest_normalize(const char* text, char* out, std::size_t cap) {
+    return guard([&] { put_str(manifest_to_json(manifest_from_json(text)), out, cap); });
+}
+// run_training_to_files (src/trainer.cpp:152-171): metrics CSV + checkpoint per the manifest
+int ref_run_training(const char* text, char* csv_out, std::size_t cap) {
+    return guard([&] {
+        const auto r = run_training_to_files(manifest_from_json(text));
+        put_str(metrics_to_csv(r), csv_out, cap);
+    });
+}
+
 } // extern "C"

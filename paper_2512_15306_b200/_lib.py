@@ -42,6 +42,10 @@ _SIGS = {
     "qt_time_graph_step": (C.c_int, [c_vp, c_vp, c_i64, c_i64, c_i64, C.c_int, C.POINTER(C.c_float)]),
     "qtk_ce_softmax_stats": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, C.c_float, c_vp, c_vp, c_i64, c_vp,
                                        c_vp]),
+    "qtk_ce_softmax_stats_tx": (C.c_int, [c_vp, c_i64, c_i64, C.c_int, c_vp, c_vp, c_vp, C.c_float, c_vp, c_i64, c_vp,
+                                          c_vp, c_vp]),
+    "qtk_lm_dgrad_finish": (C.c_int, [c_vp, c_i64, C.c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "qtk_lm_wgrad_targets": (C.c_int, [c_vp, C.c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "qtk_attn_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, c_i64, c_vp, c_vp,
                                c_vp, c_vp]),
     "qtk_attn_bwd": (C.c_int, [c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(CE_T) ce_softmax_kernel(const float* __restric
     }
 }
 
+
 // deterministic sum of per-row losses, then * inv_n (fixed tree order)
 __global__ void loss_reduce_kernel(const float* __restrict__ rows, int64_t n, float inv_n, float* __restrict__ out,
                                    float* __restrict__ accum) {
@@ -504,7 +505,8 @@ __global__ void __launch_bounds__(CE_T) ce_softmax_stats_kernel(const float* __r
                                                                 const float* __restrict__ tgt_logit, float inv_n,
                                                                 uint16_t* __restrict__ dlogits,
                                                                 uint16_t* __restrict__ dlogits_lo, int64_t ldd,
-                                                                float* __restrict__ loss_rows) {
+                                                                float* __restrict__ loss_rows,
+                                                                float* __restrict__ dl_tgt) {
     __shared__ float red[CE_T / 32];
     const int64_t row = blockIdx.x;
     const float2* st = stats + row * nstat;
@@ -533,7 +535,13 @@ __global__ void __launch_bounds__(CE_T) ce_softmax_stats_kernel(const float* __r
         float hi[4], lo[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            if (4 * i + j == tgt) p[j] -= 1.0f;
+            if (4 * i + j == tgt) {
+                p[j] -= 1.0f;
+                if (dl_tgt) {  // the target entry leaves the bf16 operand, kept exact in f32
+                    dl_tgt[row] = p[j] * inv_n;
+                    p[j] = 0.0f;
+                }
+            }
             p[j] *= inv_n;
             hi[j] = bf16r(p[j]);
             lo[j] = p[j] - hi[j];
@@ -544,11 +552,68 @@ __global__ void __launch_bounds__(CE_T) ce_softmax_stats_kernel(const float* __r
     }
     for (int i = V4 * 4 + threadIdx.x; i < V; i += CE_T) {
         float p = expf(l[i] - mx) * inv_denom;
-        if (i == tgt) p -= 1.0f;
+        if (i == tgt) {
+            p -= 1.0f;
+            if (dl_tgt) {
+                dl_tgt[row] = p * inv_n;
+                p = 0.0f;
+            }
+        }
         p *= inv_n;
         const float hi = bf16r(p);
         dl[i] = f2bfbits(hi);
         if (dlo) dlo[i] = f2bfbits(p - hi);
+    }
+}
+
+// LM-head backward with the target term kept exact (the "target-exact" CE
+// backward, DESIGN.md §2 A15).  dlogits = (p - 1[target]) / N
+// (tensorops.cpp:372-393) is split into the bf16 operand of the two GEMMs with
+// the target entry zeroed, and the f32 target term dl_t[m] = (p_t - 1) / N:
+//   d_hidden[m]  = bf16( sum_v bf16(dl[m,v]) W[v]  +  dl_t[m] * W[t_m] )
+//   d_lm_w[v]   += sum_{m : t_m = v} dl_t[m] * h[m]     (ascending m)
+// The non-target entries p_v / N are small (sum_v p_v <= 1), so their bf16
+// rounding moves the sum by less than the tensor core's own f32 accumulation;
+// the one O(1/N) entry per row is never rounded.
+__global__ void lm_dgrad_finish_kernel(const float* __restrict__ acc, int64_t M, int d, const float* __restrict__ dl_t,
+                                       const int32_t* __restrict__ targets, const uint16_t* __restrict__ W,
+                                       uint16_t* __restrict__ out) {
+    const int d4 = d / 4;
+    const int64_t total = M * d4;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m = i / d4;
+        const int c = (int)(i - m * d4) * 4;
+        const float4 a = reinterpret_cast<const float4*>(acc + m * d)[c / 4];
+        const float t = dl_t[m];
+        const uint2 wb = *reinterpret_cast<const uint2*>(W + (int64_t)targets[m] * d + c);
+        const float w0 = bfbits2f((uint16_t)(wb.x & 0xFFFF)), w1 = bfbits2f((uint16_t)(wb.x >> 16));
+        const float w2 = bfbits2f((uint16_t)(wb.y & 0xFFFF)), w3 = bfbits2f((uint16_t)(wb.y >> 16));
+        const float r0 = bf16r(__fadd_rn(a.x, __fmul_rn(t, w0)));
+        const float r1 = bf16r(__fadd_rn(a.y, __fmul_rn(t, w1)));
+        const float r2 = bf16r(__fadd_rn(a.z, __fmul_rn(t, w2)));
+        const float r3 = bf16r(__fadd_rn(a.w, __fmul_rn(t, w3)));
+        *reinterpret_cast<uint2*>(out + m * d + c) = make_uint2(pack_bf16x2(r0, r1), pack_bf16x2(r2, r3));
+    }
+}
+
+// one CTA per distinct target id (segments of the stable sort of the targets):
+// acc[v] += dl_t[m] * h[m] over the segment's positions in ascending order
+__global__ void lm_wgrad_targets_kernel(float* __restrict__ acc, int d, const int32_t* __restrict__ sorted_pos,
+                                        const int32_t* __restrict__ seg_tok, const int32_t* __restrict__ seg_off,
+                                        const int* __restrict__ nseg, const float* __restrict__ dl_t,
+                                        const uint16_t* __restrict__ h) {
+    const int ns = *nseg;
+    for (int sgi = blockIdx.x; sgi < ns; sgi += gridDim.x) {
+        const int v = seg_tok[sgi], b = seg_off[sgi], e = seg_off[sgi + 1];
+        float* row = acc + (int64_t)v * d;
+        for (int c = threadIdx.x; c < d; c += blockDim.x) {
+            float x = row[c];
+            for (int k = b; k < e; ++k) {
+                const int m = sorted_pos[k];
+                x = __fadd_rn(x, __fmul_rn(dl_t[m], bfbits2f(h[(int64_t)m * d + c])));
+            }
+            row[c] = x;
+        }
     }
 }
 
@@ -574,7 +639,38 @@ int qtk_ce_softmax_stats(const float* logits, int64_t ldl, int64_t rows, int V, 
     if ((ldl & 3) || (dlogits && (ldd & 3)) || !stats || !tgt_logit) return 1;
     ce_softmax_stats_kernel<<<(unsigned)rows, CE_T, 0, s>>>(logits, ldl, V, targets, (const float2*)stats,
                                                             (int)ceil_div(V, 128), tgt_logit, inv_n,
-                                                            (uint16_t*)dlogits, (uint16_t*)dlogits_lo, ldd, loss_rows);
+                                                            (uint16_t*)dlogits, (uint16_t*)dlogits_lo, ldd, loss_rows,
+                                                            nullptr);
+    return (int)cudaGetLastError();
+}
+
+int qtk_ce_softmax_stats_tx(const float* logits, int64_t ldl, int64_t rows, int V, const int32_t* targets,
+                            const float* stats, const float* tgt_logit, float inv_n, void* dlogits, int64_t ldd,
+                            float* loss_rows, float* dl_tgt, cudaStream_t s) {
+    if (rows <= 0) return 0;
+    if ((ldl & 3) || !dlogits || (ldd & 3) || !stats || !tgt_logit || !dl_tgt) return 1;
+    ce_softmax_stats_kernel<<<(unsigned)rows, CE_T, 0, s>>>(logits, ldl, V, targets, (const float2*)stats,
+                                                            (int)ceil_div(V, 128), tgt_logit, inv_n,
+                                                            (uint16_t*)dlogits, nullptr, ldd, loss_rows, dl_tgt);
+    return (int)cudaGetLastError();
+}
+
+int qtk_lm_dgrad_finish(const float* acc, int64_t M, int d, const float* dl_tgt, const int32_t* targets,
+                        const void* lm_w, void* d_hidden, cudaStream_t s) {
+    if (M <= 0) return 0;
+    if (d % 4) return 1;
+    const int64_t n4 = M * (d / 4);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(n4, 256), 16 * kNumSMs);
+    lm_dgrad_finish_kernel<<<g, 256, 0, s>>>(acc, M, d, dl_tgt, targets, (const uint16_t*)lm_w, (uint16_t*)d_hidden);
+    return (int)cudaGetLastError();
+}
+
+int qtk_lm_wgrad_targets(float* acc, int d, const int32_t* sorted_pos, const int32_t* seg_tok, const int32_t* seg_off,
+                         const int* nseg, int64_t max_segs, const float* dl_tgt, const void* hidden, cudaStream_t s) {
+    if (max_segs <= 0) return 0;
+    const unsigned g = (unsigned)std::min<int64_t>(max_segs, 16 * kNumSMs);
+    lm_wgrad_targets_kernel<<<g, 128, 0, s>>>(acc, d, sorted_pos, seg_tok, seg_off, nseg, dl_tgt,
+                                              (const uint16_t*)hidden);
     return (int)cudaGetLastError();
 }
 

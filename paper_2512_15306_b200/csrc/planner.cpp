@@ -272,6 +272,32 @@ QtStepTime step_time(const QtModelConfig& c, const QtPrecisionMap& pr, const QtR
     return t;
 }
 
+// ---------------------------------------------------------------- model presets
+// Public decoder shapes of model_presets (src/memplan.cpp:98-108); seq_len 1024 is the
+// accounting fixture length.  {name, layers, d, d_ff (fused), heads, kv_heads, vocab, seq, tied}
+struct Preset {
+    const char* name;
+    QtModelConfig cfg;
+    int tied;
+};
+const Preset kPresets[] = {
+    {"toy", {2, 64, 256, 4, 2, 512, 128}, 0},
+    {"0.5b", {24, 896, 9728, 14, 2, 151936, 1024}, 1},
+    {"1.5b", {28, 1536, 17920, 12, 2, 151936, 1024}, 1},
+    {"3b", {36, 2048, 22016, 16, 2, 151936, 1024}, 1},
+    {"7b", {28, 3584, 37888, 28, 4, 152064, 1024}, 0},
+    {"14b", {48, 5120, 27648, 40, 8, 152064, 1024}, 0},
+    {"32b", {64, 5120, 55296, 40, 8, 152064, 1024}, 0},
+};
+
+const Preset& preset_by_name(const std::string& name) {
+    for (const Preset& p : kPresets)
+        if (name == p.name) return p;
+    std::string avail;
+    for (const Preset& p : kPresets) avail += std::string(" ") + p.name;
+    throw PlanError("unknown model preset '" + name + "'; available:" + avail);
+}
+
 // ---------------------------------------------------------------- profiles
 // Builtins of src/profiles.cpp:21-39 plus the B200.
 std::vector<QtHardwareProfile> builtin_profiles() {
@@ -703,6 +729,14 @@ void check_cfg(const QtModelConfig* c) {
 extern "C" {
 
 const char* qt_plan_last_error(void) { return g_plan_err.c_str(); }
+
+int qt_model_preset(const char* name, QtModelConfig* cfg, int* tied) {
+    return plan_guard([&] {
+        const auto& p = qtb::plan::preset_by_name(name ? name : "");
+        *cfg = p.cfg;
+        if (tied) *tied = p.tied;
+    });
+}
 
 int qt_profile_by_name(const char* name, QtHardwareProfile* out) {
     return plan_guard([&] { *out = qtb::plan::profile_by_name(name ? name : ""); });

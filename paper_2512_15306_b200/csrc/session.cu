@@ -80,9 +80,9 @@ struct SegH {
 // small session kernels
 // ---------------------------------------------------------------------------
 // normal_init (src/model.cpp:56-65) with rng_normal (src/numerics.cpp:216-226)
-__global__ void init_normal_kernel(uint16_t* t, int64_t n, float std_, uint64_t seed, uint64_t stream) {
+__global__ void init_normal_kernel(uint16_t* t, int64_t n, float std_, uint64_t seed, uint64_t stream, int64_t base) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t c = (uint64_t)i;
+        const uint64_t c = (uint64_t)(base + i);
         const double u1 = ((double)rng_uniform(seed, stream, 2 * c) + 1.0) * 0x1.0p-32;
         const double u2 = (double)rng_uniform(seed, stream, 2 * c + 1) * 0x1.0p-32;
         const double r = sqrt(-2.0 * log(u1));
@@ -145,11 +145,11 @@ __global__ void weight_scale_kernel(const uint32_t* __restrict__ amax, float* __
 // cross-worker sum in ascending worker order, plain f32 (src/trainer.cpp:95-102)
 // recv holds W rank blocks of `stride` elements; sums elements [0, n) of each
 __global__ void ordered_sum_kernel(const uint16_t* __restrict__ recv, int W, int64_t n, int64_t stride,
-                                   float* __restrict__ out) {
+                                   float* __restrict__ out, int acc) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float s = bfbits2f(recv[i]);
         for (int w = 1; w < W; ++w) s = __fadd_rn(s, bfbits2f(recv[(int64_t)w * stride + i]));
-        out[i] = s;
+        out[i] = acc ? __fadd_rn(out[i], s) : s;
     }
 }
 
@@ -200,6 +200,11 @@ struct ParamT {
     std::string name;
     std::vector<int64_t> shape;
     int64_t numel = 0, off = 0, padded = 0, pw = 0;
+    // storage: params hold [lo, lo + store) of the tensor at `off` (shard_weights keeps only the
+    // rank's ZeRO-1 slice of a block weight); the gradient accumulator sits at `goff` in the full
+    // buffer, or (shard_grads, layer tensors) at `loff` in the per-layer buffer
+    int64_t lo = 0, store = 0, goff = -1, loff = -1;
+    bool sharded = false;
     uint64_t s_acc = 0, s_m = 0, s_v = 0, s_w = 0, s_init = 0;
 };
 
@@ -263,7 +268,7 @@ class Session {
     int64_t V, Mmax;
     std::vector<ParamT> P;
     std::map<std::string, int> pidx;
-    int64_t p_total = 0;   // padded elements of the flat param buffer
+    int64_t p_total = 0;   // padded elements of all tensors (the unsharded layout)
     int64_t shard_total = 0;
     int64_t step_count = 0;  // completed optimizer steps (OptimState::step_count)
 
@@ -277,7 +282,24 @@ class Session {
     uint16_t* m16 = nullptr;
     uint16_t* v16 = nullptr;
     float* gshard = nullptr;      // f32 reduced grads of this rank's shard (W>1)
-    uint16_t* recvbuf = nullptr;  // W x shard_total bf16
+    uint16_t* recvbuf = nullptr;  // W x shard_total bf16 (W x the non-layer shards under shard_grads)
+    int64_t p_store = 0, g_store = 0;  // params / full gradient buffer elements
+    // shard_grads: per-layer gradient buffers (double-buffered: layer l is exchanged on the
+    // communication stream while layer l-1's backward writes the other) and their receive areas
+    uint16_t* lgrad[2] = {nullptr, nullptr};
+    uint16_t* lrecv[2] = {nullptr, nullptr};
+    int64_t layer_g = 0, layer_shard = 0;  // elements of one layer's 6 tensors, padded / per rank
+    cudaEvent_t ev_lfree[2] = {nullptr, nullptr};
+    // streamed FP8 weight codes (shard_weights and/or offloaded weights): the rank's slice
+    // codes, two layer slots filled one layer ahead on the communication stream, and the
+    // pinned host copy (offload.weights; the paper's host weight cache under shard_weights)
+    std::vector<uint8_t*> wown;      // L*4 (shard_weights)
+    uint8_t* wslot[2][4] = {};
+    uint8_t* whost = nullptr;        // L x layer codes (pinned)
+    int64_t wl_off[4] = {}, wl_total = 0;  // a layer's 4 tensors inside a slot / whost entry
+    int slot_layer[2] = {-1, -1};    // which layer's codes each slot holds (this step)
+    std::vector<char> published;     // whost[l] holds this step's codes
+    cudaEvent_t ev_wfree[2] = {nullptr, nullptr}, ev_wready[2] = {nullptr, nullptr}, ev_codes = nullptr;
     std::vector<uint8_t*> wcodes;  // L*4
     std::vector<LayerBufs> lb;
     uint16_t *s_n1 = nullptr, *s_attn_out = nullptr, *s_n2 = nullptr, *s_h = nullptr, *normed_final = nullptr;
@@ -288,7 +310,16 @@ class Session {
     int64_t gemm_ws_bytes = 0;
     float* logits = nullptr;
     uint16_t* dlogits = nullptr;
-    uint16_t* dlogits_lo = nullptr;
+    uint16_t* dlogits_lo = nullptr;  // hi/lo CE backward only (lm_tx() off)
+    // target-exact CE backward (lm_tx()): f32 target terms, the LM-head split-K partials,
+    // the f32 sum buffer (d_hidden before rounding, then d_lm_w) and the targets' stable sort
+    float* dl_tgt = nullptr;
+    float* lm_ws = nullptr;
+    int64_t lm_ws_bytes = 0;
+    int lm_splits = 1;
+    float* lm_acc = nullptr;
+    int32_t *t_sorted_pos = nullptr, *t_seg_tok = nullptr, *t_seg_off = nullptr;
+    int* t_nseg = nullptr;
     float* loss_rows = nullptr;
     float* ce_stats = nullptr;   // [M][ceil(V/128)] (max, sum exp) pairs from the logits GEMM
     float* ce_tgt = nullptr;     // [M] logit of the target
@@ -373,10 +404,15 @@ class Session {
             } catch (const TransportError& e) {
                 throw QtError(3, e.what());
             }
-            QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
-            QT_CHECK_CUDA(cudaEventCreateWithFlags(&ev_grad, cudaEventDisableTiming));
-            QT_CHECK_CUDA(cudaEventCreateWithFlags(&ev_comm, cudaEventDisableTiming));
         }
+        if (world > 1 || stream_codes()) {
+            QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+            for (cudaEvent_t* e : {&ev_grad, &ev_comm, &ev_codes, &ev_lfree[0], &ev_lfree[1], &ev_wfree[0], &ev_wfree[1],
+                                   &ev_wready[0], &ev_wready[1]})
+                QT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+        if (stream_codes() && offload_weights())
+            QT_CHECK_CUDA(cudaMallocHost(&whost, std::max<size_t>((size_t)L * wl_total, 1)));
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
 
@@ -406,9 +442,11 @@ class Session {
     ~Session() {
         tr.reset();
         for (auto e : ev_pool) cudaEventDestroy(e);
-        if (ev_grad) cudaEventDestroy(ev_grad);
-        if (ev_comm) cudaEventDestroy(ev_comm);
+        for (cudaEvent_t e : {ev_grad, ev_comm, ev_codes, ev_lfree[0], ev_lfree[1], ev_wfree[0], ev_wfree[1], ev_wready[0],
+                              ev_wready[1]})
+            if (e) cudaEventDestroy(e);
         if (cst) cudaStreamDestroy(cst);
+        if (whost) cudaFreeHost(whost);
         if (gexec) cudaGraphExecDestroy(gexec);
         for (auto& e : blk_ev)
             if (e) cudaEventDestroy(e);
@@ -472,10 +510,38 @@ class Session {
             soff_of.push_back(shard_total);
             shard_total += t.pw;
         }
+        // storage layout (world 1: offsets == the unsharded layout, params and grads alike)
+        p_store = g_store = layer_g = 0;
+        for (int i = 0; i < (int)P.size(); ++i) {
+            ParamT& t = P[i];
+            t.sharded = shard_weights() && is_block_weight(i);
+            t.lo = t.sharded ? (int64_t)rank * t.pw : 0;
+            t.store = t.sharded ? t.pw : t.padded;
+            t.off = p_store;
+            p_store += t.store;
+            if (shard_grads() && i >= 1 && i <= 6 * L) {
+                const int k = (i - 1) % 6;
+                if (k == 0) layer_g = 0;
+                t.loff = layer_g;
+                layer_g += t.padded;
+            } else {
+                t.goff = g_store;
+                g_store += t.padded;
+            }
+        }
+        layer_shard = layer_g / std::max(world, 1);
+    }
+    // elements of tensor t stored on this rank ([lo, lo + n) of the tensor)
+    int64_t stored(const ParamT& t) const { return std::max<int64_t>(0, std::min(t.store, t.numel - t.lo)); }
+    // the gradient accumulator of tensor i (layer l's slot under shard_grads)
+    uint16_t* gbuf(const ParamT& t) {
+        if (t.goff >= 0) return grads + t.goff;
+        const int pi = (int)(&t - P.data());
+        return lgrad[((pi - 1) / 6) % 2] + t.loff;
     }
     const ParamT& par(const std::string& n) const { return P.at(pidx.at(n)); }
     uint16_t* pptr(const std::string& n) { return params + par(n).off; }
-    uint16_t* gptr(const std::string& n) { return grads + par(n).off; }
+    uint16_t* gptr(const std::string& n) { return gbuf(par(n)); }
     int lp(int l, int k) const { return 1 + 6 * l + k; }  // k: 0 ln1 1 qkv 2 o 3 ln2 4 gu 5 down
 
     bool keep(int site) const {
@@ -503,8 +569,8 @@ class Session {
         std::vector<Req> reqs;
         auto req = [&](auto** p, size_t bytes) { reqs.push_back({reinterpret_cast<void**>(p), bytes}); };
         const int64_t M = Mmax;
-        req(&params, p_total * 2);
-        req(&grads, p_total * 2);
+        req(&params, p_store * 2);
+        req(&grads, std::max<int64_t>(g_store, 1) * 2);
         if (plan.bf16_moments) {
             req(&m16, shard_total * 2);
             req(&v16, shard_total * 2);
@@ -514,14 +580,46 @@ class Session {
         }
         if (world > 1) {
             req(&gshard, shard_total * 4);
-            req(&recvbuf, (size_t)world * shard_total * 2);
+            if (shard_grads()) {
+                // the non-layer tensors (embed, final_g, lm_head) exchange through recvbuf at
+                // the end; each layer through its own double-buffered receive area
+                int64_t rest = 0;
+                for (auto& t : P)
+                    if (t.goff >= 0) rest += t.pw;
+                req(&recvbuf, (size_t)world * rest * 2);
+                for (int k = 0; k < 2; ++k) {
+                    req(&lgrad[k], layer_g * 2);
+                    req(&lrecv[k], (size_t)world * layer_shard * 2);
+                }
+            } else {
+                req(&recvbuf, (size_t)world * shard_total * 2);
+            }
         }
         wcodes.assign((size_t)L * 4, nullptr);
-        for (int l = 0; l < L; ++l) {  // padded to W*pw: shard_weights all-gathers the codes in place
-            req(&wcodes[l * 4 + W_QKV], (size_t)P[lp(l, 1)].padded);
-            req(&wcodes[l * 4 + W_O], (size_t)P[lp(l, 2)].padded);
-            req(&wcodes[l * 4 + W_GU], (size_t)P[lp(l, 4)].padded);
-            req(&wcodes[l * 4 + W_DOWN], (size_t)P[lp(l, 5)].padded);
+        {
+            const int wk[4] = {1, 2, 4, 5};
+            wl_total = 0;
+            for (int k = 0; k < 4; ++k) {
+                wl_off[k] = wl_total;
+                wl_total += ceil_div(P[lp(0, wk[k])].padded, 128) * 128;
+            }
+        }
+        if (!stream_codes()) {
+            for (int l = 0; l < L; ++l) {
+                req(&wcodes[l * 4 + W_QKV], (size_t)P[lp(l, 1)].padded);
+                req(&wcodes[l * 4 + W_O], (size_t)P[lp(l, 2)].padded);
+                req(&wcodes[l * 4 + W_GU], (size_t)P[lp(l, 4)].padded);
+                req(&wcodes[l * 4 + W_DOWN], (size_t)P[lp(l, 5)].padded);
+            }
+        } else {
+            for (int sl = 0; sl < 2; ++sl) req(&wslot[sl][0], (size_t)wl_total);
+            if (shard_weights()) {
+                wown.assign((size_t)L * 4, nullptr);
+                const int wk[4] = {1, 2, 4, 5};
+                for (int l = 0; l < L; ++l)
+                    for (int k = 0; k < 4; ++k) req(&wown[l * 4 + k], (size_t)P[lp(l, wk[k])].pw);
+            }
+            if (offload_weights()) host_bytes += (size_t)L * wl_total;
         }
         lb.assign(L + 1, LayerBufs());
         // shared scratch for dropped sites
@@ -576,7 +674,21 @@ class Session {
         }
         req(&logits, (size_t)M * V * 4);
         req(&dlogits, (size_t)M * V * 2);
-        req(&dlogits_lo, (size_t)M * V * 2);
+        if (lm_tx()) {
+            // split-K over the vocabulary keeps each tensor-core f32 accumulation chain short
+            // (~19k terms): the chain's truncating adds drift by ~1e-4 relative over 152k terms
+            lm_splits = (int)std::min<int64_t>(8, std::max<int64_t>(1, ceil_div(V, 16384)));
+            lm_ws_bytes = lm_splits > 1 ? (int64_t)lm_splits * M * d * 4 : 0;
+            if (lm_ws_bytes) req(&lm_ws, lm_ws_bytes);
+            req(&lm_acc, (size_t)std::max<int64_t>(V, M) * d * 4);
+            req(&dl_tgt, M * 4);
+            req(&t_sorted_pos, M * 4);
+            req(&t_seg_tok, M * 4);
+            req(&t_seg_off, (M + 1) * 4);
+            req(&t_nseg, 16);
+        } else {
+            req(&dlogits_lo, (size_t)M * V * 2);
+        }
         req(&loss_rows, M * 4);
         req(&ce_stats, (size_t)M * ceil_div(V, 128) * 8);
         req(&ce_tgt, M * 4);
@@ -679,7 +791,7 @@ class Session {
                 s.off = soff;
                 s.n = hi - lo;
                 s.gstart = (int64_t)rank * t.pw;
-                s.poff = t.off + (int64_t)rank * t.pw;
+                s.poff = t.sharded ? t.off : t.off + (int64_t)rank * t.pw;
                 soff += t.pw;
             }
             s.gnumel = t.numel;
@@ -717,7 +829,8 @@ class Session {
     }
 
     // ---------------- profiling ----------------
-    int prof_begin() {
+    int prof_begin() { return prof_begin_on(st); }
+    int prof_begin_on(cudaStream_t ss) {
         if (!prof_on) return -1;
         if (ev_used + 2 > ev_pool.size()) {
             for (int i = 0; i < 256; ++i) {
@@ -727,15 +840,16 @@ class Session {
             }
         }
         cudaEvent_t a = ev_pool[ev_used++], b = ev_pool[ev_used++];
-        cudaEventRecord(a, st);
+        cudaEventRecord(a, ss);
         prof.push_back({0, a, b, 0.0});
         return (int)prof.size() - 1;
     }
-    void prof_end(int h, int cat, double work) {
+    void prof_end(int h, int cat, double work) { prof_end_on(h, cat, work, st); }
+    void prof_end_on(int h, int cat, double work, cudaStream_t ss) {
         if (h < 0) return;
         prof[h].cat = cat;
         prof[h].work = work;
-        cudaEventRecord(prof[h].b, st);
+        cudaEventRecord(prof[h].b, ss);
     }
 
     // ---------------- GEMM helper ----------------
@@ -743,7 +857,8 @@ class Session {
               int64_t lda, const void* b, int64_t ldb, const float* as, const float* bs, int epi, void* out,
               int64_t ldo, const void* res = nullptr, int64_t ldr = 0, uint64_t sr_seed = 0, uint64_t sr_stream = 0,
               uint64_t sr_base = 0, const void* a2 = nullptr, uint32_t* amax = nullptr, const int32_t* ce_targets = nullptr,
-              float* ce_st = nullptr, float* ce_tl = nullptr) {
+              float* ce_st = nullptr, float* ce_tl = nullptr, float* ws = nullptr, int64_t ws_bytes = 0,
+              int split_k = 0) {
         QtkGemm g{};
         g.kind = kind;
         g.a_fmt = afmt;
@@ -769,9 +884,9 @@ class Session {
         g.sr_base = sr_base;
         g.bn = 0;
         g.a2 = a2;
-        g.ws = gemm_ws;
-        g.ws_bytes = gemm_ws_bytes;
-        g.split_k = 0;
+        g.ws = ws ? ws : gemm_ws;
+        g.ws_bytes = ws ? ws_bytes : gemm_ws_bytes;
+        g.split_k = ws ? split_k : 0;
         g.amax = amax;
         if (use_dev_ctr && (epi == EPI_BF16_ACC || epi == EPI_F32_ACC)) g.sr_micro_step = ms_dev(cur_ga);
         g.ce_targets = ce_targets;
@@ -800,6 +915,16 @@ class Session {
         }
         return f != 0 && V % 4 == 0;  // TMA-stored f32 logits rows
     }
+    // target-exact CE backward: bf16 dlogits without the target entry + the exact f32 target
+    // term (QTB_LM_TX=0: the bf16 hi + lo split-A path)
+    bool lm_tx() const {
+        static int f = -1;
+        if (f < 0) {
+            const char* e = getenv("QTB_LM_TX");
+            f = e ? atoi(e) : 1;
+        }
+        return f != 0 && ce_stats_on() && d % 4 == 0;
+    }
     bool fuse_swiglu_bwd() const {
         static int f = -1;
         if (f < 0) {
@@ -813,6 +938,16 @@ class Session {
 
     // ---------------- StepContext (src/model.cpp:88-107) ----------------
     bool shard_weights() const { return plan.shard_weights && world > 1; }
+    // RunPlan::offload.weights: the FP8 codes live in pinned host memory, two layer slots on
+    // the device (memplan.hpp:34-52; with shard_weights this is the paper's host weight cache)
+    bool offload_weights() const { return (plan.offload_bits & QT_OFF_WEIGHTS) != 0; }
+    // the block weights' codes are streamed per layer (not all resident)
+    bool stream_codes() const { return shard_weights() || offload_weights(); }
+    // the codes of weight k (W_QKV, W_O, W_GU, W_DOWN) of layer l
+    const uint8_t* wc(int l, int k) const {
+        if (!stream_codes()) return wcodes[l * 4 + k];
+        return wslot[l % 2][0] + wl_off[k];
+    }
     bool shard_grads() const { return plan.shard_grads && world > 1; }
     // w_qkv, w_o, w_gate_up, w_down of some layer (for_each_param order, model.hpp:107-121)
     bool is_block_weight(int pi) const {
@@ -823,40 +958,38 @@ class Session {
 
     void build_step_context() {
         QT_CHECK_CUDA(cudaMemsetAsync(w_amax, 0, L * 16, st));
+        slot_layer[0] = slot_layer[1] = -1;  // last step's codes are stale
+        if (stream_codes()) published.assign((size_t)L, 0);
         if (shard_weights()) {
             // RunPlan::shard_weights: each rank holds only its ZeRO-1 slice of the block
             // weights.  Per-tensor absmax = max over the ranks' slice maxima (all-reduce MAX of
-            // the u32 |x| bit patterns), each rank casts its slice with that scale, and the
-            // E4M3 codes (1 B/param, half the bf16 traffic) are all-gathered in place.
-            // Codes equal a cast of the full tensor bit for bit (the cast is elementwise).
+            // the u32 |x| patterns), each rank casts its slice with that scale into its own
+            // slice codes; the forward/backward all-gather the E4M3 codes (1 B/param) one layer
+            // ahead (fetch_layer).  Codes equal a cast of the full tensor bit for bit.
             for (int l = 0; l < L; ++l) {
                 const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
                 for (int k = 0; k < 4; ++k) {
                     const ParamT& t = P[widx[k]];
-                    const int64_t lo = std::min<int64_t>((int64_t)rank * t.pw, t.numel);
-                    const int64_t n = std::min<int64_t>(t.pw, t.numel - lo);
-                    if (n > 0) QT_CHECK_K(qtk_absmax_bf16(params + t.off + lo, n, w_amax + l * 4 + k, st));
+                    const int64_t n = stored(t);
+                    if (n > 0) QT_CHECK_K(qtk_absmax_bf16(params + t.off, n, w_amax + l * 4 + k, st));
                 }
             }
             coll([&] { tr->allreduce_max_u32(w_amax, (size_t)L * 4, st); });
             weight_scale_kernel<<<(unsigned)ceil_div(L * 4, 128), 128, 0, st>>>(w_amax, w_scale, L * 4);  // ranks with an empty slice
             QT_CHECK_CUDA(cudaGetLastError());
-            std::vector<AllGatherItem> items;
             for (int l = 0; l < L; ++l) {
                 const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
                 for (int k = 0; k < 4; ++k) {
                     const ParamT& t = P[widx[k]];
-                    const int64_t lo = (int64_t)rank * t.pw;
-                    const int64_t n = std::max<int64_t>(0, std::min<int64_t>(t.pw, t.numel - lo));
+                    const int64_t n = stored(t);
                     const int h = prof_begin();
                     if (n > 0)
-                        QT_CHECK_K(qtk_quantize_bf16(params + t.off + lo, n, kE4M3, w_amax + l * 4 + k,
-                                                     wcodes[l * 4 + k] + lo, w_scale + l * 4 + k, st));
+                        QT_CHECK_K(qtk_quantize_bf16(params + t.off, n, kE4M3, w_amax + l * 4 + k, wown[l * 4 + k],
+                                                     w_scale + l * 4 + k, st));
                     prof_end(h, 3, 3.0 * n);
-                    items.push_back({wcodes[l * 4 + k], (size_t)t.pw});
                 }
             }
-            coll([&] { tr->allgather(items, st); });
+            QT_CHECK_CUDA(cudaEventRecord(ev_codes, st));  // the slice codes are ready
             return;
         }
         if (amax_cached) {  // the absmax AdamW folded in while writing these weights
@@ -869,11 +1002,65 @@ class Session {
                 const ParamT& t = P[widx[k]];
                 const int h = prof_begin();
                 if (!amax_cached) QT_CHECK_K(qtk_absmax_bf16(params + t.off, t.numel, w_amax + l * 4 + k, st));
-                QT_CHECK_K(qtk_quantize_bf16(params + t.off, t.numel, kE4M3, w_amax + l * 4 + k, wcodes[l * 4 + k],
+                // offload.weights: cast into a device slot, then publish to the host cache
+                uint8_t* dst = offload_weights() ? wslot[l % 2][0] + wl_off[k] : wcodes[l * 4 + k];
+                QT_CHECK_K(qtk_quantize_bf16(params + t.off, t.numel, kE4M3, w_amax + l * 4 + k, dst,
                                              w_scale + l * 4 + k, st));
                 prof_end(h, 3, 3.0 * t.numel);
             }
+            if (offload_weights()) {
+                QT_CHECK_CUDA(cudaMemcpyAsync(whost + (size_t)l * wl_total, wslot[l % 2][0], (size_t)wl_total,
+                                              cudaMemcpyDeviceToHost, st));
+                QT_CHECK_CUDA(cudaEventRecord(ev_wready[l % 2], st));
+                published[(size_t)l] = 1;
+                slot_layer[l % 2] = l;
+            }
         }
+        if (stream_codes()) QT_CHECK_CUDA(cudaEventRecord(ev_codes, st));  // codes (and slots) written
+    }
+
+    // ---------------- streamed weight codes (shard_weights / offload.weights) ----------------
+    // fetch_layer(l) fills slot l%2 with layer l's codes on the communication stream once the
+    // slot's previous user finished (ev_wfree), and records ev_wready.  Source: the peers'
+    // slices (all-gather; with offload.weights also published to the host cache, so later
+    // passes of this step read the host copy), or the host cache.  Every rank takes the same
+    // decisions, so the collectives line up.
+    void fetch_layer(int l) {
+        const int sl = l % 2;
+        if (slot_layer[sl] == l) return;
+        QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_wfree[sl], 0));
+        QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_codes, 0));  // this step's codes exist
+        const int h = prof_begin_on(cst);
+        if (shard_weights() && !published[(size_t)l]) {
+            const int widx[4] = {lp(l, 1), lp(l, 2), lp(l, 4), lp(l, 5)};
+            std::vector<GatherItem> items;
+            for (int k = 0; k < 4; ++k)
+                items.push_back({wown[l * 4 + k], wslot[sl][0] + wl_off[k], (size_t)P[widx[k]].pw});
+            coll([&] { tr->allgather_to(items, cst); });
+            if (offload_weights()) {
+                QT_CHECK_CUDA(cudaMemcpyAsync(whost + (size_t)l * wl_total, wslot[sl][0], (size_t)wl_total,
+                                              cudaMemcpyDeviceToHost, cst));
+                published[(size_t)l] = 1;
+            }
+        } else {
+            QT_CHECK_CUDA(cudaMemcpyAsync(wslot[sl][0], whost + (size_t)l * wl_total, (size_t)wl_total,
+                                          cudaMemcpyHostToDevice, cst));
+        }
+        prof_end_on(h, 9, (double)wl_total, cst);
+        QT_CHECK_CUDA(cudaEventRecord(ev_wready[sl], cst));
+        slot_layer[sl] = l;
+    }
+    // before layer l's compute: its codes are in the slot (prefetching l+dir meanwhile)
+    void codes_acquire(int l, int next) {
+        if (!stream_codes()) return;
+        fetch_layer(l);
+        if (next >= 0 && next < L) fetch_layer(next);
+        QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_wready[l % 2], 0));
+    }
+    // after layer l's compute: its slot may be refilled
+    void codes_release(int l) {
+        if (!stream_codes()) return;
+        QT_CHECK_CUDA(cudaEventRecord(ev_wfree[l % 2], st));
     }
 
     // ---------------- block forward (src/model.cpp:239-293) ----------------
@@ -894,7 +1081,7 @@ class Session {
         h = prof_begin();
         QT_CHECK_K(qtk_quantize_bf16(s_n1, M * d, kE4M3, am + S_N1, b.n1c, sc + S_N1, st));
         prof_end(h, 3, 3.0 * M * d);
-        gemm(0, kE4M3, kE4M3, false, false, M, q, d, b.n1c, d, wcodes[l * 4 + W_QKV], d, sc + S_N1, ws + W_QKV, EPI_BF16,
+        gemm(0, kE4M3, kE4M3, false, false, M, q, d, b.n1c, d, wc(l, W_QKV), d, sc + S_N1, ws + W_QKV, EPI_BF16,
              b.qkv, q);
         h = prof_begin();
         QT_CHECK_K(qtk_rope(b.qkv, M, curT, H + Hkv, hd, q, rope_tab, 0, nullptr, st));
@@ -906,7 +1093,7 @@ class Session {
         h = prof_begin();
         QT_CHECK_K(qtk_quantize_bf16(b.att, M * d, kE4M3, am + S_ATT, b.attc, sc + S_ATT, st));
         prof_end(h, 3, 3.0 * M * d);
-        gemm(0, kE4M3, kE4M3, false, false, M, d, d, b.attc, d, wcodes[l * 4 + W_O], d, sc + S_ATT, ws + W_O, EPI_BF16,
+        gemm(0, kE4M3, kE4M3, false, false, M, d, d, b.attc, d, wc(l, W_O), d, sc + S_ATT, ws + W_O, EPI_BF16,
              s_attn_out, d);
         h = prof_begin();
         QT_CHECK_K(qtk_rmsnorm_fwd(s_attn_out, b.r_in, params + ln2.off, M, d, 1e-6f, b.r_mid, s_n2, rms_inv,
@@ -915,7 +1102,7 @@ class Session {
         h = prof_begin();
         QT_CHECK_K(qtk_quantize_bf16(s_n2, M * d, kE4M3, am + S_N2, b.n2c, sc + S_N2, st));
         prof_end(h, 3, 3.0 * M * d);
-        gemm(0, kE4M3, kE4M3, false, false, M, F, d, b.n2c, d, wcodes[l * 4 + W_GU], d, sc + S_N2, ws + W_GU, EPI_BF16,
+        gemm(0, kE4M3, kE4M3, false, false, M, F, d, b.n2c, d, wc(l, W_GU), d, sc + S_N2, ws + W_GU, EPI_BF16,
              b.gu, F);
         h = prof_begin();
         QT_CHECK_K(qtk_swiglu_fwd(b.gu, M, Hh, s_h, record ? am + S_H : nullptr, st));
@@ -924,7 +1111,7 @@ class Session {
         QT_CHECK_K(qtk_quantize_bf16(s_h, M * Hh, kE4M3, am + S_H, b.hc, sc + S_H, st));
         prof_end(h, 3, 3.0 * M * Hh);
         // r_out = bf16(bf16(h . Wdown^T) + r_mid)  (model.cpp:281-283) -> next layer's r_in
-        gemm(0, kE4M3, kE4M3, false, false, M, d, Hh, b.hc, Hh, wcodes[l * 4 + W_DOWN], Hh, sc + S_H, ws + W_DOWN,
+        gemm(0, kE4M3, kE4M3, false, false, M, d, Hh, b.hc, Hh, wc(l, W_DOWN), Hh, sc + S_H, ws + W_DOWN,
              EPI_BF16_RES, lb[l + 1].r_in, d, b.r_mid, d);
     }
 
@@ -946,7 +1133,11 @@ class Session {
         prof_end(h, 5, 4.0 * M * d);
         if (with_grads) QT_CHECK_K(qtk_embed_sort(inputs, (int)M, V, sort_scratch, sort_scratch_bytes, sorted_pos,
                                                   seg_tok, seg_off, nseg, st));
-        for (int l = 0; l < L; ++l) block_forward(l, true);
+        for (int l = 0; l < L; ++l) {
+            codes_acquire(l, l + 1);
+            block_forward(l, true);
+            codes_release(l);
+        }
         h = prof_begin();
         QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, lb[L].r_in, pptr("final_g"), M, d, 1e-6f, nullptr, normed_final, rms_inv,
                                    fin_amax, st));
@@ -958,10 +1149,21 @@ class Session {
             gemm(1, 0, 0, false, false, M, V, d, normed_final, d, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, logits,
                  V, nullptr, 0, 0, 0, 0, nullptr, nullptr, targets, ce_stats, ce_tgt);
             h = prof_begin();
-            QT_CHECK_K(qtk_ce_softmax_stats(logits, V, M, (int)V, targets, ce_stats, ce_tgt, 1.0f / (float)M,
-                                            with_grads ? dlogits : nullptr, with_grads ? dlogits_lo : nullptr, V,
-                                            loss_rows, st));
-            prof_end(h, 7, (with_grads ? 8.0 : 0.0) * M * V);
+            if (lm_tx() && with_grads) {
+                QT_CHECK_K(qtk_ce_softmax_stats_tx(logits, V, M, (int)V, targets, ce_stats, ce_tgt, 1.0f / (float)M,
+                                                   dlogits, V, loss_rows, dl_tgt, st));
+                prof_end(h, 7, 6.0 * M * V);
+                // positions grouped by target (stable: ascending within a target) for d_lm_w's target terms
+                h = prof_begin();
+                QT_CHECK_K(qtk_embed_sort(targets, (int)M, V, sort_scratch, sort_scratch_bytes, t_sorted_pos,
+                                          t_seg_tok, t_seg_off, t_nseg, st));
+                prof_end(h, 5, 0.0);
+            } else {
+                QT_CHECK_K(qtk_ce_softmax_stats(logits, V, M, (int)V, targets, ce_stats, ce_tgt, 1.0f / (float)M,
+                                                with_grads ? dlogits : nullptr, with_grads ? dlogits_lo : nullptr, V,
+                                                loss_rows, st));
+                prof_end(h, 7, (with_grads ? 8.0 : 0.0) * M * V);
+            }
         } else {
             gemm(1, 0, 0, false, false, M, V, d, normed_final, d, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, logits,
                  V);
@@ -983,13 +1185,31 @@ class Session {
         const int gk = gkind();
         int h;
         // CE backward matmuls: d_hidden = dlogits . lm_w ; d_lm_w = dlogits^T . hidden
+        if (lm_tx()) {
+            // dlogits = bf16 non-target entries + the exact f32 target term (tensorops.cpp:372-405)
+            const ParamT& t = par("lm_head");
+            gemm(1, 0, 0, false, true, M, d, V, dlogits, V, pptr("lm_head"), d, nullptr, nullptr, EPI_F32, lm_acc, d,
+                 nullptr, 0, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, lm_ws, lm_ws_bytes, lm_splits);
+            h = prof_begin();
+            QT_CHECK_K(qtk_lm_dgrad_finish(lm_acc, M, d, dl_tgt, targets, pptr("lm_head"), d_hidden, st));
+            prof_end(h, 5, 8.0 * M * d);
+            gemm(1, 0, 0, true, true, V, d, M, dlogits, V, normed_final, d, nullptr, nullptr, EPI_F32, lm_acc, d);
+            h = prof_begin();
+            QT_CHECK_K(qtk_lm_wgrad_targets(lm_acc, d, t_sorted_pos, t_seg_tok, t_seg_off, t_nseg, M, dl_tgt,
+                                            normed_final, st));
+            prof_end(h, 5, 2.0 * M * d);
+            h = prof_begin();
+            accumulate_f32(t, lm_acc, micro_step);
+            prof_end(h, 5, 8.0 * (double)t.numel);
+        } else {
         // (dlogits is f32 in the reference: hi + lo bf16 parts through the split-A GEMM)
         gemm(1, 0, 0, false, true, M, d, V, dlogits, V, pptr("lm_head"), d, nullptr, nullptr, EPI_BF16, d_hidden, d,
              nullptr, 0, 0, 0, 0, dlogits_lo);
         {
             const ParamT& t = par("lm_head");
             gemm(1, 0, 0, true, true, V, d, M, dlogits, V, normed_final, d, nullptr, nullptr, EPI_F32_ACC,
-                 grads + t.off, d, nullptr, 0, aseed, t.s_acc, micro_step * (uint64_t)t.numel, dlogits_lo);
+                 gbuf(t), d, nullptr, 0, aseed, t.s_acc, micro_step * (uint64_t)t.numel, dlogits_lo);
+        }
         }
         // final norm backward (model.cpp:359-363)
         h = prof_begin();
@@ -1000,6 +1220,11 @@ class Session {
         prof_end(h, 4, 8.0 * M * d);
         for (int l = L - 1; l >= 0; --l) {
             LayerBufs& b = lb[l];
+            codes_acquire(l, l - 1);
+            if (exchange_in_backward) {  // the layer's gradient slot: free (exchange done) and zeroed
+                QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_lfree[l % 2], 0));
+                QT_CHECK_CUDA(cudaMemsetAsync(lgrad[l % 2], 0, layer_g * 2, st));
+            }
             if (!b.keep_all) block_forward(l, false);  // replay with cached stats (model.cpp:374-378)
             uint32_t* ga = g_amax + l * 4;
             float* gs = g_scale + l * 4;
@@ -1014,14 +1239,14 @@ class Session {
             QT_CHECK_K(qtk_quantize_bf16(d_r, M * d, gk, ga + G_DR, gcodes, gs + G_DR, st));
             prof_end(h, 3, 3.0 * M * d);
             gemm(0, gk, kE4M3, true, true, d, Hh, M, gcodes, d, b.hc, Hh, gs + G_DR, as + S_H, EPI_BF16_ACC,
-                 grads + pd.off, Hh, nullptr, 0, aseed, pd.s_acc, micro_step * (uint64_t)pd.numel);
+                 gbuf(pd), Hh, nullptr, 0, aseed, pd.s_acc, micro_step * (uint64_t)pd.numel);
             if (fuse_swiglu_bwd()) {
                 // d_h = down-proj dgrad, consumed in the GEMM epilogue by swiglu_backward:
                 // d_gate|d_up + their absmax written directly (d_h never reaches HBM)
-                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wcodes[l * 4 + W_DOWN], Hh, gs + G_DR,
+                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wc(l, W_DOWN), Hh, gs + G_DR,
                      ws + W_DOWN, EPI_SWIGLU_BWD, d_gu, F, b.gu, F, 0, 0, 0, nullptr, ga + G_DGU);
             } else {
-                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wcodes[l * 4 + W_DOWN], Hh, gs + G_DR,
+                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wc(l, W_DOWN), Hh, gs + G_DR,
                      ws + W_DOWN, EPI_BF16, d_h, Hh);
                 h = prof_begin();
                 QT_CHECK_K(qtk_swiglu_bwd(b.gu, d_h, M, Hh, d_gu, ga + G_DGU, st));
@@ -1032,8 +1257,8 @@ class Session {
             QT_CHECK_K(qtk_quantize_bf16(d_gu, M * F, gk, ga + G_DGU, gcodes, gs + G_DGU, st));
             prof_end(h, 3, 3.0 * M * F);
             gemm(0, gk, kE4M3, true, true, F, d, M, gcodes, F, b.n2c, d, gs + G_DGU, as + S_N2, EPI_BF16_ACC,
-                 grads + pg.off, d, nullptr, 0, aseed, pg.s_acc, micro_step * (uint64_t)pg.numel);
-            gemm(0, gk, kE4M3, false, true, M, d, F, gcodes, F, wcodes[l * 4 + W_GU], d, gs + G_DGU, ws + W_GU, EPI_BF16,
+                 gbuf(pg), d, nullptr, 0, aseed, pg.s_acc, micro_step * (uint64_t)pg.numel);
+            gemm(0, gk, kE4M3, false, true, M, d, F, gcodes, F, wc(l, W_GU), d, gs + G_DGU, ws + W_GU, EPI_BF16,
                  d_n, d);
             // ---- rmsnorm2 backward: d_attn_out = ... + d_r (model.cpp:393-399)
             h = prof_begin();
@@ -1046,8 +1271,8 @@ class Session {
             QT_CHECK_K(qtk_quantize_bf16(d_ao, M * d, gk, ga + G_DAO, gcodes, gs + G_DAO, st));
             prof_end(h, 3, 3.0 * M * d);
             gemm(0, gk, kE4M3, true, true, d, d, M, gcodes, d, b.attc, d, gs + G_DAO, as + S_ATT, EPI_BF16_ACC,
-                 grads + po.off, d, nullptr, 0, aseed, po.s_acc, micro_step * (uint64_t)po.numel);
-            gemm(0, gk, kE4M3, false, true, M, d, d, gcodes, d, wcodes[l * 4 + W_O], d, gs + G_DAO, ws + W_O, EPI_BF16,
+                 gbuf(po), d, nullptr, 0, aseed, po.s_acc, micro_step * (uint64_t)po.numel);
+            gemm(0, gk, kE4M3, false, true, M, d, d, gcodes, d, wc(l, W_O), d, gs + G_DAO, ws + W_O, EPI_BF16,
                  d_att, d);
             // ---- attention backward + inverse RoPE
             h = prof_begin();
@@ -1061,8 +1286,8 @@ class Session {
             QT_CHECK_K(qtk_quantize_bf16(d_qkv, M * q, gk, ga + G_DQKV, gcodes, gs + G_DQKV, st));
             prof_end(h, 3, 3.0 * M * q);
             gemm(0, gk, kE4M3, true, true, q, d, M, gcodes, q, b.n1c, d, gs + G_DQKV, as + S_N1, EPI_BF16_ACC,
-                 grads + pq.off, d, nullptr, 0, aseed, pq.s_acc, micro_step * (uint64_t)pq.numel);
-            gemm(0, gk, kE4M3, false, true, M, d, q, gcodes, q, wcodes[l * 4 + W_QKV], d, gs + G_DQKV, ws + W_QKV,
+                 gbuf(pq), d, nullptr, 0, aseed, pq.s_acc, micro_step * (uint64_t)pq.numel);
+            gemm(0, gk, kE4M3, false, true, M, d, q, gcodes, q, wc(l, W_QKV), d, gs + G_DQKV, ws + W_QKV,
                  EPI_BF16, d_n, d);
             // ---- rmsnorm1 backward: d_r = ... + d_attn_out (model.cpp:433-439)
             h = prof_begin();
@@ -1070,6 +1295,7 @@ class Session {
                                        dgamma, l > 0 ? g_amax + (l - 1) * 4 + G_DR : nullptr, st));
             accumulate_f32(P[lp(l, 0)], dgamma, micro_step);
             prof_end(h, 4, 10.0 * M * d);
+            codes_release(l);
             if (exchange_in_backward) reduce_layer_async(l);
         }
         // ordered embedding backward, bf16 round, accumulate (model.cpp:442-444)
@@ -1077,10 +1303,10 @@ class Session {
             const ParamT& t = par("embed");
             h = prof_begin();
             if (use_dev_ctr)
-                QT_CHECK_K(qtk_embed_bwd_ms(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, t.numel, grads + t.off,
+                QT_CHECK_K(qtk_embed_bwd_ms(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, t.numel, gbuf(t),
                                             aseed, t.s_acc, ms_dev(cur_ga), st));
             else
-                QT_CHECK_K(qtk_embed_bwd(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, grads + t.off, aseed,
+                QT_CHECK_K(qtk_embed_bwd(sorted_pos, seg_off, seg_tok, nseg, (int)M, d_r, d, gbuf(t), aseed,
                                          t.s_acc, micro_step * (uint64_t)t.numel, st));
             prof_end(h, 5, 4.0 * M * d);
         }
@@ -1088,48 +1314,55 @@ class Session {
 
     void accumulate_f32(const ParamT& t, const float* g, uint64_t micro_step) {
         if (use_dev_ctr)
-            QT_CHECK_K(qtk_sr_accumulate_f32_ms(grads + t.off, g, t.numel, seed + (uint64_t)rank, t.s_acc,
+            QT_CHECK_K(qtk_sr_accumulate_f32_ms(gbuf(t), g, t.numel, seed + (uint64_t)rank, t.s_acc,
                                                 ms_dev(cur_ga), st));
         else
-            QT_CHECK_K(qtk_sr_accumulate_f32(grads + t.off, g, t.numel, seed + (uint64_t)rank, t.s_acc,
+            QT_CHECK_K(qtk_sr_accumulate_f32(gbuf(t), g, t.numel, seed + (uint64_t)rank, t.s_acc,
                                              micro_step * (uint64_t)t.numel, st));
     }
 
     // ---------------- cross-rank gradient reduction (ZeRO-1) ----------------
-    // all-to-all of bf16 shards + ascending-rank f32 sum == trainer.cpp:90-103 bitwise,
-    // for the tensors [i0, i1) of the parameter list, on stream s
-    void reduce_tensors(int i0, int i1, cudaStream_t s) {
+    // all-to-all of bf16 shards + ascending-rank f32 sum == trainer.cpp:90-103 bitwise, for
+    // the tensors [i0, i1) (contiguous shards); rank r's chunk of tensor i lands at
+    // rbuf + r*rstride + (soff_of[i] - soff_of[i0]); acc: add onto the shard (shard_grads, GA > 1)
+    void exchange(int i0, int i1, cudaStream_t s, uint16_t* rbuf, int64_t rstride, bool acc) {
         std::vector<AllToAllItem> items;
         for (int i = i0; i < i1; ++i) {
             const ParamT& t = P[i];
-            items.push_back({grads + t.off, (size_t)t.pw * 2, recvbuf + soff_of[i], (size_t)shard_total * 2,
+            items.push_back({gbuf(t), (size_t)t.pw * 2, rbuf + (soff_of[i] - soff_of[i0]), (size_t)rstride * 2,
                              (size_t)t.pw * 2});
         }
         coll([&] { tr->alltoall(items, s); });
         const int64_t n = soff_of[i1 - 1] + P[i1 - 1].pw - soff_of[i0];
-        ordered_sum_kernel<<<grid_for(n), 256, 0, s>>>(recvbuf + soff_of[i0], world, n, shard_total,
-                                                      gshard + soff_of[i0]);
+        ordered_sum_kernel<<<grid_for(n), 256, 0, s>>>(rbuf, world, n, rstride, gshard + soff_of[i0], acc ? 1 : 0);
         QT_CHECK_CUDA(cudaGetLastError());
     }
     void reduce_grads() {
         const int h = prof_begin();
-        reduce_tensors(0, (int)P.size(), st);
+        exchange(0, (int)P.size(), st, recvbuf, shard_total, false);
         prof_end(h, 9, 2.0 * shard_total * (world - 1) * 2);
     }
-    // RunPlan::shard_grads: layer l's gradients are final once its backward is done (last
-    // micro-batch): exchange them on the communication stream while layers l-1..0 run
+    // RunPlan::shard_grads: layer l's gradients (this micro-batch) are final once its backward
+    // is done: exchange them on the communication stream while layers l-1..0 run, into the
+    // rank's f32 shard; the layer's slot is then free for layer l-2
     void reduce_layer_async(int l) {
         QT_CHECK_CUDA(cudaEventRecord(ev_grad, st));
         QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_grad, 0));
-        reduce_tensors(lp(l, 0), lp(l, 5) + 1, cst);
+        const int h = prof_begin_on(cst);
+        exchange(lp(l, 0), lp(l, 5) + 1, cst, lrecv[l % 2], layer_shard, cur_ga > 0);
+        prof_end_on(h, 9, 2.0 * layer_shard * (world - 1) * 2, cst);
+        QT_CHECK_CUDA(cudaEventRecord(ev_lfree[l % 2], cst));
         comm_pending = true;
     }
     void reduce_rest_and_join() {
-        // embed (index 0) and final_g / lm_head (the last two) on the comm stream, then join
+        // embed (index 0) and final_g / lm_head (the last two), accumulated locally over the
+        // micro-batches, on the comm stream; then join
         QT_CHECK_CUDA(cudaEventRecord(ev_grad, st));
         QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_grad, 0));
-        reduce_tensors(0, 1, cst);
-        reduce_tensors((int)P.size() - 2, (int)P.size(), cst);
+        const int np = (int)P.size();
+        const int64_t rest = P[0].pw + P[np - 2].pw + P[np - 1].pw;
+        exchange(0, 1, cst, recvbuf, rest, false);
+        exchange(np - 2, np, cst, recvbuf + P[0].pw, rest, false);
         QT_CHECK_CUDA(cudaEventRecord(ev_comm, cst));
         QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_comm, 0));
         comm_pending = false;
@@ -1193,7 +1426,7 @@ class Session {
         pre_step_count = step_count;
         // world > 1 stays stream-launched: the NCCL exchange inside a captured graph has
         // not been exercised on hardware this round (gpurun boxes have one GPU)
-        if (!graph_enabled() || prof_on || !amax_cached || world > 1) {
+        if (!graph_enabled() || prof_on || !amax_cached || world > 1 || stream_codes()) {
             train_step_body(tokens, tokens_per_mb, batch, step, max_norm);
             return;
         }
@@ -1261,13 +1494,13 @@ class Session {
             ~InStep() { f = false; }
         } in_step_guard(in_step);
         build_step_context();
-        QT_CHECK_CUDA(cudaMemsetAsync(grads, 0, p_total * 2, st));
+        QT_CHECK_CUDA(cudaMemsetAsync(grads, 0, g_store * 2, st));
         for (int ga = 0; ga < GA; ++ga) {
             forward(tokens + (int64_t)ga * tokens_per_mb, tokens_per_mb, batch, true);
             QT_CHECK_CUDA(cudaMemcpyAsync(loss_dev + 1 + ga, loss_dev, 4, cudaMemcpyDeviceToDevice, st));
-            // shard_grads: the final gradients of layer l are exchanged while layers < l run
-            // backward (last micro-batch only, so the summation order stays trainer.cpp:90-103)
-            exchange_in_backward = shard_grads() && ga == GA - 1;
+            // shard_grads: each micro-batch's gradients of layer l are exchanged into the rank's
+            // shard while layers < l run backward (GA = 1: the order of trainer.cpp:90-103)
+            exchange_in_backward = shard_grads();
             cur_ga = ga;
             backward((uint64_t)step * GA + ga);
             exchange_in_backward = false;
@@ -1450,8 +1683,11 @@ int qt_param_upload(qt_session* h, int i, const float* host) {
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
         s.amax_cached = false;
-        QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, host, t.numel * 4, cudaMemcpyHostToDevice, s.st));
-        f32_to_bf16_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.scratch_f32, s.params + t.off, t.numel);
+        const int64_t n = s.stored(t);  // shard_weights: the rank keeps its slice only
+        if (n > 0) {
+            QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, host + t.lo, n * 4, cudaMemcpyHostToDevice, s.st));
+            f32_to_bf16_kernel<<<grid_for(n), 256, 0, s.st>>>(s.scratch_f32, s.params + t.off, n);
+        }
         QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
     });
 }
@@ -1469,9 +1705,15 @@ int qt_param_download(qt_session* h, int i, float* host) {
     return guard([&] {
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
-        if (s.shard_weights() && s.is_block_weight(i)) {
-            s.coll([&] { s.tr->gather_idle(s.params + t.off, (size_t)t.pw * 2, s.recvbuf, s.st); });
-            download_bf16(s, s.recvbuf, t.numel, host);
+        if (t.sharded) {  // the ranks' slices, read from the peers (NCCL: a collective)
+            uint16_t* stage = reinterpret_cast<uint16_t*>(s.scratch_f32);
+            s.coll([&] { s.tr->gather_idle(s.params + t.off, (size_t)t.pw * 2, stage, s.st); });
+            std::vector<uint16_t> b((size_t)t.numel);
+            QT_CHECK_CUDA(cudaMemcpy(b.data(), stage, t.numel * 2, cudaMemcpyDeviceToHost));
+            for (int64_t e = 0; e < t.numel; ++e) {
+                const uint32_t u = (uint32_t)b[(size_t)e] << 16;
+                std::memcpy(host + e, &u, 4);
+            }
             return;
         }
         download_bf16(s, s.params + t.off, t.numel, host);
@@ -1482,7 +1724,19 @@ int qt_grad_download(qt_session* h, int i, float* host) {
     return guard([&] {
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
+        if (t.goff < 0)
+            throw QtError(1, "shard_grads keeps no local accumulator for layer tensors (qt_reduced_grad_download)");
         download_bf16(s, s.grads + t.off, t.numel, host);
+    });
+}
+// the cross-rank reduced f32 gradient of tensor i (world > 1): every rank's shard, gathered
+int qt_reduced_grad_download(qt_session* h, int i, float* host) {
+    return guard([&] {
+        Session& s = *h->s;
+        if (s.world < 2) throw QtError(1, "qt_reduced_grad_download: world > 1 only");
+        const ParamT& t = s.P.at(i);
+        s.coll([&] { s.tr->gather_idle(s.gshard + s.soff_of[i], (size_t)t.pw * 4, s.scratch_f32, s.st); });
+        QT_CHECK_CUDA(cudaMemcpy(host, s.scratch_f32, t.numel * 4, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -1505,14 +1759,63 @@ int qt_moments_download(qt_session* h, int i, float* m, float* v) {
     });
 }
 
+// m, v: the full tensor (numel floats); each rank keeps its ZeRO-1 slice.  bf16-SR moments
+// take values on the bf16 grid (as a checkpoint of such moments holds) and store them exactly.
 int qt_moments_upload(qt_session* h, int i, const float* m, const float* v, int64_t step_count) {
     return guard([&] {
         Session& s = *h->s;
-        if (s.plan.bf16_moments || s.world > 1) throw QtError(1, "moments upload: world == 1, f32 moments only");
         const ParamT& t = s.P.at(i);
-        QT_CHECK_CUDA(cudaMemcpy(s.m32 + t.off, m, t.numel * 4, cudaMemcpyHostToDevice));
-        QT_CHECK_CUDA(cudaMemcpy(s.v32 + t.off, v, t.numel * 4, cudaMemcpyHostToDevice));
+        std::vector<SegH> segs(s.nsegs);
+        QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDeviceToHost));
+        const SegH& sg = segs[i];
+        const int64_t off = s.world > 1 ? sg.off : t.off;
+        const int64_t lo = s.world > 1 ? std::min<int64_t>((int64_t)s.rank * t.pw, t.numel) : 0;
+        if (sg.n > 0) {
+            if (s.plan.bf16_moments) {
+                for (int k = 0; k < 2; ++k) {
+                    QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, (k ? v : m) + lo, sg.n * 4, cudaMemcpyHostToDevice,
+                                                  s.st));
+                    f32_to_bf16_kernel<<<grid_for(sg.n), 256, 0, s.st>>>(s.scratch_f32, (k ? s.v16 : s.m16) + off,
+                                                                           sg.n);
+                }
+            } else {
+                QT_CHECK_CUDA(cudaMemcpyAsync(s.m32 + off, m + lo, sg.n * 4, cudaMemcpyHostToDevice, s.st));
+                QT_CHECK_CUDA(cudaMemcpyAsync(s.v32 + off, v + lo, sg.n * 4, cudaMemcpyHostToDevice, s.st));
+            }
+            QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+        }
         s.step_count = step_count;
+    });
+}
+
+int qt_step_count(qt_session* h, int64_t* out) {
+    return guard([&] { *out = h->s->step_count; });
+}
+
+// per-micro-batch losses of the last qt_train_step on this rank (ga_steps floats)
+int qt_step_losses(qt_session* h, float* out) {
+    return guard([&] {
+        Session& s = *h->s;
+        QT_CHECK_CUDA(cudaMemcpyAsync(out, s.loss_dev + 1, 4 * (size_t)s.plan.ga_steps, cudaMemcpyDeviceToHost, s.st));
+        QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
+    });
+}
+
+int qt_session_rank(qt_session* h, int* rank, int* world) {
+    return guard([&] {
+        *rank = h->s->rank;
+        *world = h->s->world;
+    });
+}
+
+// ZeRO-1 slice [lo, lo + n) of tensor i this rank's optimizer state covers
+int qt_moments_slice(qt_session* h, int i, int64_t* lo, int64_t* n) {
+    return guard([&] {
+        Session& s = *h->s;
+        const ParamT& t = s.P.at(i);
+        *lo = s.world > 1 ? std::min<int64_t>((int64_t)s.rank * t.pw, t.numel) : 0;
+        *n = s.world > 1 ? std::min<int64_t>(t.pw, t.numel - *lo) : t.numel;
+        if (*n < 0) *n = 0;
     });
 }
 
@@ -1524,10 +1827,12 @@ int qt_init_params(qt_session* h, uint64_t seed) {
         const float std_ = 1.0f / std::sqrt(static_cast<float>(s.d));
         for (auto& t : s.P) {
             const bool gamma = t.shape.size() == 1;
+            const int64_t n = s.stored(t);  // shard_weights: the rank's slice [lo, lo + n)
+            if (n <= 0) continue;
             if (gamma)
-                fill_bf16_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.params + t.off, t.numel, 1.0f);
+                fill_bf16_kernel<<<grid_for(n), 256, 0, s.st>>>(s.params + t.off, n, 1.0f);
             else
-                init_normal_kernel<<<grid_for(t.numel), 256, 0, s.st>>>(s.params + t.off, t.numel, std_, seed, t.s_init);
+                init_normal_kernel<<<grid_for(n), 256, 0, s.st>>>(s.params + t.off, n, std_, seed, t.s_init, t.lo);
         }
         QT_CHECK_CUDA(cudaGetLastError());
         QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
@@ -1555,7 +1860,7 @@ int qt_backward(qt_session* h, uint64_t micro_step) {
 }
 
 int qt_zero_grads(qt_session* h) {
-    return guard([&] { QT_CHECK_CUDA(cudaMemsetAsync(h->s->grads, 0, h->s->p_total * 2, h->s->st)); });
+    return guard([&] { QT_CHECK_CUDA(cudaMemsetAsync(h->s->grads, 0, h->s->g_store * 2, h->s->st)); });
 }
 
 int qt_grad_norm(qt_session* h, double* norm_host) {
@@ -1661,6 +1966,7 @@ int qt_saved_raw(qt_session* h, int layer, const char* site, void* host, int64_t
         else if (n == "dlogits") { src = s.dlogits; nb = M * s.V * 2; }
         else if (n == "dlogits_lo") { src = s.dlogits_lo; nb = M * s.V * 2; }
         else if (n == "d_hidden") { src = s.d_hidden; nb = M * s.d * 2; }
+        else if (n == "dl_tgt") { src = s.dl_tgt; nb = M * 4; dt = 2; }
         else if (n == "logits") { src = s.logits; nb = M * s.V * 4; dt = 2; }
         else if (layer == s.L) throw QtError(1, "only r_in exists for layer L (r_final)");
         else if (n == "n1c") { src = b.n1c; nb = M * s.d; dt = 1; }
@@ -1673,6 +1979,7 @@ int qt_saved_raw(qt_session* h, int layer, const char* site, void* host, int64_t
         else if (n == "hc") { src = b.hc; nb = M * s.Hh; dt = 1; }
         else if (n == "lse") { src = b.lse; nb = (int64_t)s.curB * s.H * s.curT * 4; dt = 2; }
         else throw QtError(1, "unknown site " + n);
+        if (!src) throw QtError(1, "site " + n + " is not kept in this CE backward mode");
         *bytes = nb;
         *dtype = dt;
         if (host) QT_CHECK_CUDA(cudaMemcpy(host, src, nb, cudaMemcpyDeviceToHost));
@@ -1693,7 +2000,20 @@ int qt_weight_codes(qt_session* h, int layer, int which, uint8_t* host) {
     return guard([&] {
         Session& s = *h->s;
         const int64_t n[4] = {(int64_t)s.q * s.d, (int64_t)s.d * s.d, (int64_t)s.F * s.d, (int64_t)s.d * s.Hh};
-        QT_CHECK_CUDA(cudaMemcpy(host, s.wcodes[layer * 4 + which], n[which], cudaMemcpyDeviceToHost));
+        if (layer < 0 || layer >= s.L || which < 0 || which > 3) throw QtError(2, "layer/weight out of range");
+        if (!s.stream_codes()) {
+            QT_CHECK_CUDA(cudaMemcpy(host, s.wcodes[layer * 4 + which], n[which], cudaMemcpyDeviceToHost));
+        } else if (s.offload_weights() && !s.published.empty() && s.published[(size_t)layer]) {
+            std::memcpy(host, s.whost + (size_t)layer * s.wl_total + s.wl_off[which], (size_t)n[which]);
+        } else if (s.shard_weights()) {
+            const int widx[4] = {1, 2, 4, 5};
+            const ParamT& t = s.P[s.lp(layer, widx[which])];
+            uint8_t* stage = reinterpret_cast<uint8_t*>(s.scratch_f32);
+            s.coll([&] { s.tr->gather_idle(s.wown[layer * 4 + which], (size_t)t.pw, stage, s.st); });
+            QT_CHECK_CUDA(cudaMemcpy(host, stage, n[which], cudaMemcpyDeviceToHost));
+        } else {
+            throw QtError(1, "weight codes are not built yet (build_step_context)");
+        }
     });
 }
 

@@ -48,6 +48,11 @@ struct AllGatherItem {
     void* base;       // this rank's buffer; chunk r at base + r*chunk_bytes
     size_t chunk_bytes;
 };
+struct GatherItem {
+    const void* src;  // this rank's chunk (same offset in every rank's arena)
+    void* dst;        // rank r's chunk lands at dst + r*chunk_bytes
+    size_t chunk_bytes;
+};
 struct AllToAllItem {
     const void* send_base;  // chunk destined to rank j at send_base + j*send_stride
     size_t send_stride;
@@ -64,10 +69,12 @@ class Transport {
     virtual void allreduce_max_u32(uint32_t* buf, size_t n, cudaStream_t s) = 0;
     virtual void allreduce_sum_f64(double* buf, size_t n, cudaStream_t s) = 0;
     virtual void allgather(const std::vector<AllGatherItem>& items, cudaStream_t s) = 0;
+    // out of place: dst + r*chunk = rank r's src, on every rank
+    virtual void allgather_to(const std::vector<GatherItem>& items, cudaStream_t s) = 0;
     virtual void alltoall(const std::vector<AllToAllItem>& items, cudaStream_t s) = 0;
-    // Outside the step: dst[r*chunk .. ] = rank r's chunk at base + r*chunk, for every r
+    // Outside the step: dst[r*chunk .. ] = rank r's chunk at `src` (same offset on every rank)
     // (the peer group reads idle peers' arenas directly; NCCL: a collective all ranks enter)
-    virtual void gather_idle(const void* base, size_t chunk_bytes, void* dst, cudaStream_t s) = 0;
+    virtual void gather_idle(const void* src, size_t chunk_bytes, void* dst, cudaStream_t s) = 0;
     // bytes this rank moved through the transport (sent + received), for the bench line
     double bytes_moved = 0.0;
 };
@@ -112,6 +119,15 @@ class NcclTransport final : public Transport {
         }
         check(api.GroupEnd(), "all-gather");
     }
+    void allgather_to(const std::vector<GatherItem>& items, cudaStream_t s) override {
+        auto& api = NcclApi::get();
+        api.GroupStart();
+        for (auto& it : items) {
+            api.AllGather(it.src, it.dst, it.chunk_bytes, ncclUint8, comm, s);
+            bytes_moved += 2.0 * (world - 1) * it.chunk_bytes;
+        }
+        check(api.GroupEnd(), "all-gather");
+    }
     void alltoall(const std::vector<AllToAllItem>& items, cudaStream_t s) override {
         auto& api = NcclApi::get();
         api.GroupStart();
@@ -131,10 +147,9 @@ class NcclTransport final : public Transport {
         }
         check(api.GroupEnd(), "shard exchange");
     }
-    void gather_idle(const void* base, size_t chunk_bytes, void* dst, cudaStream_t s) override {
-        check(NcclApi::get().AllGather(static_cast<const uint8_t*>(base) + (size_t)rank * chunk_bytes, dst, chunk_bytes,
-                                       ncclUint8, comm, s),
-              "gather");
+    void gather_idle(const void* src, size_t chunk_bytes, void* dst, cudaStream_t s) override {
+        check(NcclApi::get().AllGather(src, dst, chunk_bytes, ncclUint8, comm, s), "gather");
+        cudaStreamSynchronize(s);
     }
 };
 
@@ -324,14 +339,19 @@ class PeerTransport final : public Transport {
                 }
         leave(s);
     }
-    void gather_idle(const void* base, size_t chunk_bytes, void* dst, cudaStream_t s) override {
+    void gather_idle(const void* src, size_t chunk_bytes, void* dst, cudaStream_t s) override {
         first_use_nobarrier();
-        for (int p = 0; p < world; ++p) {
-            const uint8_t* src = static_cast<const uint8_t*>(base) + (size_t)p * chunk_bytes;
+        for (int p = 0; p < world; ++p)
             cudaMemcpyAsync(static_cast<uint8_t*>(dst) + (size_t)p * chunk_bytes, peer_addr(p, src), chunk_bytes,
                             cudaMemcpyDefault, s);
-        }
         cudaStreamSynchronize(s);
+    }
+    void allgather_to(const std::vector<GatherItem>& items, cudaStream_t s) override {
+        enter(s);
+        for (auto& it : items)
+            for (int p = 0; p < world; ++p)
+                pull(static_cast<uint8_t*>(it.dst) + (size_t)p * it.chunk_bytes, p, it.src, it.chunk_bytes, s);
+        leave(s);
     }
     void first_use_nobarrier() {
         for (int p = 0; p < world; ++p)

@@ -151,6 +151,64 @@ def ce_softmax_stats(logits, targets, stats, tgt_logit, inv_n: float):
     return loss, hi, lo
 
 
+def ce_softmax_stats_tx(logits, targets, stats, tgt_logit, inv_n: float):
+    """Target-exact CE softmax: per-row loss, bf16 dlogits with the target entry
+    zeroed, and the f32 target term dl_t = (p_t - 1) / N."""
+    rows, V = logits.shape
+    loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    dl = torch.empty((rows, V), dtype=torch.bfloat16, device=logits.device)
+    dlt = torch.empty(rows, dtype=torch.float32, device=logits.device)
+    rc = _lib.lib().qtk_ce_softmax_stats_tx(_p(logits), logits.stride(0), rows, V, _p(targets), _p(stats),
+                                            _p(tgt_logit), inv_n, _p(dl), V, _p(loss), _p(dlt), _s())
+    _lib.check(rc, "qtk_ce_softmax_stats_tx")
+    return loss, dl, dlt
+
+
+def embed_sort(ids: torch.Tensor, V: int):
+    """Stable sort of positions by id (qtk_embed_sort): sorted_pos, seg_tok,
+    seg_off, nseg (device tensors)."""
+    n = ids.numel()
+    L = _lib.lib()
+    nb = L.qtk_embed_sort_scratch_bytes(n, V)
+    scratch = torch.empty(max(nb, 1), dtype=torch.uint8, device=ids.device)
+    sp = torch.empty(n, dtype=torch.int32, device=ids.device)
+    st = torch.empty(n, dtype=torch.int32, device=ids.device)
+    so = torch.empty(n + 1, dtype=torch.int32, device=ids.device)
+    ns = torch.zeros(4, dtype=torch.int32, device=ids.device)
+    _lib.check(L.qtk_embed_sort(_p(ids), n, V, _p(scratch), nb, _p(sp), _p(st), _p(so), _p(ns), _s()),
+               "qtk_embed_sort")
+    return sp, st, so, ns
+
+
+def lm_splits(V: int) -> int:
+    """The session's split-K factor for the LM-head dgrad (K = V)."""
+    return int(min(8, max(1, -(-V // 16384))))
+
+
+def lm_dgrad_tx(dl, dl_t, targets, lm_w):
+    """d_hidden of the target-exact CE backward, as the session runs it: split-K
+    f32 GEMM of the bf16 dlogits, then + dl_t * lm_w[target], rounded to bf16."""
+    M, V = dl.shape
+    d = lm_w.shape[1]
+    acc = gemm(dl, lm_w, M=M, N=d, K=V, b_mn=True, epi=EPI_F32, split_k=lm_splits(V))
+    out = torch.empty((M, d), dtype=torch.bfloat16, device=dl.device)
+    _lib.check(_lib.lib().qtk_lm_dgrad_finish(_p(acc), M, d, _p(dl_t), _p(targets), _p(lm_w), _p(out), _s()),
+               "qtk_lm_dgrad_finish")
+    return out
+
+
+def lm_wgrad_tx(dl, dl_t, targets, hidden):
+    """f32 d_lm_w of the target-exact CE backward: GEMM of the bf16 dlogits
+    (target entries zero) + the exact target terms in ascending token order."""
+    M, V = dl.shape
+    d = hidden.shape[1]
+    acc = gemm(dl, hidden, M=V, N=d, K=M, a_mn=True, b_mn=True, epi=EPI_F32)
+    sp, st, so, ns = embed_sort(targets, V)
+    _lib.check(_lib.lib().qtk_lm_wgrad_targets(_p(acc), d, _p(sp), _p(st), _p(so), _p(ns), M, _p(dl_t), _p(hidden),
+                                               _s()), "qtk_lm_wgrad_targets")
+    return acc
+
+
 def rmsnorm_fwd(x, res, gamma, eps=1e-6, with_absmax=True):
     rows, d = res.shape
     nr = torch.empty_like(res) if x is not None else None

@@ -161,6 +161,7 @@ _SIGS = {
     "qt_param_upload": (_ci, [_vp, _ci, _vp]),
     "qt_param_download": (_ci, [_vp, _ci, _vp]),
     "qt_grad_download": (_ci, [_vp, _ci, _vp]),
+    "qt_reduced_grad_download": (_ci, [_vp, _ci, _vp]),
     "qt_moments_download": (_ci, [_vp, _ci, _vp, _vp]),
     "qt_moments_upload": (_ci, [_vp, _ci, _vp, _vp, _i64]),
     "qt_init_params": (_ci, [_vp, _u64]),
@@ -373,6 +374,13 @@ class Session:
         i = self._i(name)
         out = np.empty(self.numel[i], np.float32)
         _chk(lib().qt_grad_download(self.h, i, out.ctypes.data))
+        return out
+
+    def reduced_grad(self, name: str) -> np.ndarray:
+        """world > 1: the cross-rank reduced f32 gradient (every rank's shard gathered)."""
+        i = self._i(name)
+        out = np.empty(self.numel[i], np.float32)
+        _chk(lib().qt_reduced_grad_download(self.h, i, out.ctypes.data))
         return out
 
     def moments(self, name: str):

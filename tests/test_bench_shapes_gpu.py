@@ -216,60 +216,76 @@ def test_lmhead_logits_ce_stats_epilogue_bench_shape(ops, ref):
     np.testing.assert_array_equal(tl[ri].cpu().numpy(), got[np.arange(len(rows)), t[ri].long().cpu().numpy()])
 
 
-def _hi_lo(M, V, seed):
-    g = torch.Generator(device="cuda").manual_seed(seed)
-    p = torch.randn(M, V, generator=g, device="cuda") * 1e-6
-    hi = p.to(torch.bfloat16)
-    lo = (p - hi.float()).to(torch.bfloat16)
-    del p
-    return hi, lo
+def _ce_operands(ops, M, d, V, seed):
+    """The production CE operands at the bench shape: logits by the LM-head GEMM
+    with the statistics epilogue, then the target-exact softmax (bf16 dlogits
+    with the target entry zeroed + f32 target term)."""
+    h = _bf16_rand((M, d), 1.0, seed)
+    w = _bf16_rand((V, d), d ** -0.5, seed + 1)
+    t = torch.randint(0, V, (M,), dtype=torch.int32, device="cuda",
+                      generator=torch.Generator(device="cuda").manual_seed(seed + 2))
+    stats = torch.empty(M, (V + 127) // 128, 2, dtype=torch.float32, device="cuda")
+    tl = torch.empty(M, dtype=torch.float32, device="cuda")
+    logits = ops.gemm(h, w, M=M, N=V, K=d, epi=ops.EPI_F32, ce=(t, stats, tl))
+    _, dl, dlt = ops.ce_softmax_stats_tx(logits, t, stats, tl, 1.0 / M)
+    del logits, stats
+    return h, w, t, dl, dlt
 
 
-def test_lmhead_dgrad_split_a_bench_shape(ops, ref):
-    """d_hidden = dlogits . lm_w with f32 dlogits carried as bf16 hi + lo through
-    the split-A GEMM (D = A.B + A2.B), M = 16384, K = V = 151936; bf16 out vs the
-    reference's f32 matmul of (hi + lo), rounded (tensorops.cpp:394-399)."""
+def test_lmhead_dgrad_target_exact_bench_shape(ops, ref):
+    """d_hidden = bf16(sum_v dl[m,v] lm_w[v] + dl_t[m] lm_w[t_m]) at M = 16384,
+    K = V = 151936 as the session runs it (split-K f32 GEMM of the bf16 dlogits,
+    then the exact target term), vs the reference's sequential f32 matmul of
+    the same operands (tensorops.cpp:394-399): <= 1 ulp everywhere, >= 99 %
+    exact; the split-K instantiation is asserted."""
     M, d, V = Q05["M"], Q05["d"], Q05["V"]
-    hi, lo = _hi_lo(M, V, 21)
-    w = _bf16_rand((V, d), d ** -0.5, 22)
-    kw = dict(M=M, N=d, K=V, b_mn=True, epi=ops.EPI_BF16, a2=lo)
-    plan = ops.gemm_plan(hi, w, **kw)
-    assert (plan["cg"], plan["bn"]) == (2, 256) and plan["tiles_per_cta"] >= 4, plan
-    out = ops.gemm(hi, w, **kw)
+    h, w, t, dl, dlt = _ce_operands(ops, M, d, V, 21)
+    kw = dict(M=M, N=d, K=V, b_mn=True, epi=ops.EPI_F32, split_k=ops.lm_splits(V))
+    plan = ops.gemm_plan(dl, w, **kw)
+    assert (plan["cg"], plan["bn"], plan["splits"]) == (2, 256, 8) and plan["tiles_per_cta"] >= 8, plan
+    out = ops.lm_dgrad_tx(dl, dlt, t, w)
     torch.cuda.synchronize()
     rows = _rows(M, n=10, seed=4)
     ri = torch.from_numpy(rows).cuda()
-    a = (hi[ri].float() + lo[ri].float()).cpu().numpy()
+    a = dl[ri].float().cpu().numpy()
     wf = w.float().cpu().numpy()
-    want = ref.matmul_f32(a, wf.T.copy(), round_bf16=True)
-    absscale = np.abs(a).astype(np.float64) @ np.abs(wf).astype(np.float64)
+    acc = ref.matmul_f32(a, wf.T.copy(), round_bf16=False)
+    tt = t[ri].long().cpu().numpy()
+    dt = dlt[ri].cpu().numpy()
+    want = bf16_grid_round((acc + dt[:, None] * wf[tt]).astype(np.float32))
+    absscale = np.abs(a).astype(np.float64) @ np.abs(wf).astype(np.float64) + np.abs(dt[:, None] * wf[tt])
     _close(out[ri].float().cpu().numpy(), want, absscale, V, frac=0.99, what=f"lm dgrad {plan}")
 
 
-def test_lmhead_wgrad_split_a_sr_accumulate_bench_shape(ops, ref):
-    """d_lm_w = dlogits^T . normed (split-A, MN-major operands) in f32, then
-    GradAccumulator SR into the bf16 buffer (EPI_F32_ACC), V = 151936 rows,
-    K = M = 16384 tokens (tensorops.cpp:400-405; model.cpp:455-462)."""
+def test_lmhead_wgrad_target_exact_bench_shape(ops, ref):
+    """f32 d_lm_w = dl^T . normed + the exact target terms, V = 151936 rows,
+    K = M = 16384 tokens (tensorops.cpp:400-405), sampled vocabulary rows
+    (targets of many tokens included) vs the reference's f32 matmul of the same
+    operand plus the target terms in ascending token order."""
     M, d, V = Q05["M"], Q05["d"], Q05["V"]
-    hi, lo = _hi_lo(M, V, 31)
+    h, w, t, dl, dlt = _ce_operands(ops, M, d, V, 31)
     x = _bf16_rand((M, d), 1.0, 32)
-    buf = _bf16_rand((V, d), 1e-4, 33)
-    seed, stream, micro = 77, ref.fnv1a64("gradaccum/lm_head"), 2
-    kw = dict(M=V, N=d, K=M, a_mn=True, b_mn=True, epi=ops.EPI_F32_ACC, a2=lo, out=buf.clone(),
-              sr=(seed, stream, micro * V * d))
-    plan = ops.gemm_plan(hi, x, **kw)
+    kw = dict(M=V, N=d, K=M, a_mn=True, b_mn=True, epi=ops.EPI_F32)
+    plan = ops.gemm_plan(dl, x, **kw)
     assert (plan["cg"], plan["bn"]) == (2, 256) and plan["tiles_per_cta"] >= 30, plan
-    out = ops.gemm(hi, x, **kw)
+    out = ops.lm_wgrad_tx(dl, dlt, t, x)
     torch.cuda.synchronize()
-    rows = _rows(V, n=10, seed=5)
-    ri = torch.from_numpy(rows).cuda()
-    a = (hi[:, ri].float() + lo[:, ri].float()).T.contiguous().cpu().numpy()
+    tv = t.cpu().numpy()
+    vrows = np.unique(np.concatenate([tv[:6], np.random.default_rng(5).choice(V, 6, replace=False)]))
+    vi = torch.from_numpy(vrows).cuda()
+    a = dl[:, vi].float().T.contiguous().cpu().numpy()
     xf = x.float().cpu().numpy()
-    g = ref.matmul_f32(a, xf.T.copy(), round_bf16=False)
-    b0 = buf[ri].float().cpu().numpy()
-    want = _sr_ref(ref, b0, g, rows, d, seed, stream, micro * V * d)
-    absscale = np.abs(a).astype(np.float64) @ np.abs(xf).astype(np.float64) + np.abs(b0)
-    _close(out[ri].float().cpu().numpy(), want, absscale, M, frac=0.99, what=f"lm wgrad {plan}")
+    want = ref.matmul_f32(a, xf.T.copy(), round_bf16=False)
+    dtn = dlt.cpu().numpy()
+    for r, v in enumerate(vrows):
+        for m in np.nonzero(tv == v)[0]:  # ascending token order
+            want[r] = (want[r] + np.float32(dtn[m]) * xf[m]).astype(np.float32)
+    got = out[vi].cpu().numpy()
+    absscale = np.abs(a).astype(np.float64) @ np.abs(xf).astype(np.float64)
+    for r, v in enumerate(vrows):
+        absscale[r] += np.abs(dtn[tv == v, None] * xf[tv == v]).sum(axis=0)
+    tol = 8.0 * np.sqrt(M) * 2.0 ** -24 * absscale
+    assert (np.abs(got.astype(np.float64) - want) <= tol).all(), np.abs(got - want).max()
 
 
 # ---------------------------------------------------------------- attention
@@ -335,8 +351,9 @@ def test_attention_bench_shapes(ops, ref, B, T, H, Hkv, hd, kvs):
 @pytest.mark.parametrize("N,d,V", [(32, 896, 151936), (32, 4096, 32000)], ids=["qwen_vocab", "llama_vocab"])
 def test_cross_entropy_production_path_real_vocab(ops, ref, N, d, V):
     """The session's CE path — logits GEMM with the statistics epilogue, the
-    single-pass ce_softmax_stats (dlogits as bf16 hi + lo), split-A dgrad and
-    wgrad — at the real vocabularies vs fused_cross_entropy_chunked
+    single-pass target-exact softmax (bf16 dlogits without the target entry +
+    the f32 target term), split-K dgrad and the wgrad with exact target terms —
+    at the real vocabularies vs fused_cross_entropy_chunked
     (tensorops.cpp:344-410): loss 1e-5 rel, d_hidden <= 1 ulp on >= 99 %,
     d_lm_w 1e-4 rel (f32, accumulation order)."""
     g = np.random.default_rng(V + d)
@@ -350,11 +367,17 @@ def test_cross_entropy_production_path_real_vocab(ops, ref, N, d, V):
     stats = torch.empty(N, (V + 127) // 128, 2, dtype=torch.float32, device="cuda")
     tl = torch.empty(N, dtype=torch.float32, device="cuda")
     logits = ops.gemm(H, W, M=N, N=V, K=d, epi=ops.EPI_F32, ce=(T_, stats, tl))
-    lr, hi, lo = ops.ce_softmax_stats(logits, T_, stats, tl, 1.0 / N)
+    lr, dl, dlt = ops.ce_softmax_stats_tx(logits, T_, stats, tl, 1.0 / N)
     got_loss = lr.sum().item() / N
     assert abs(got_loss - loss) / loss < 1e-5, (got_loss, loss)
-    dh_g = ops.gemm(hi, W, M=N, N=d, K=V, b_mn=True, epi=ops.EPI_BF16, a2=lo).float().cpu().numpy()
+    dh_g = ops.lm_dgrad_tx(dl, dlt, T_, W).float().cpu().numpy()
+    # <= 1 ulp on >= 99.9 % (transcendental ops <= 1 ulp on >= 99 %), the rest
+    # within the cancellation-aware bound, >= 98 % bit-exact
     du = _ulp(dh_g, dh)
-    assert (du == 0).mean() > 0.99 and _rel(dh_g, dh) < 1e-3, ((du == 0).mean(), _rel(dh_g, dh))
-    dw_g = ops.gemm(hi, H, M=V, N=d, K=N, a_mn=True, b_mn=True, epi=ops.EPI_F32, a2=lo).cpu().numpy()
+    # sum_v |dl[m, v] w[v, c]| <= (|p_t - 1| + sum p_v) / N * max|w| <= 2 max|w| / N
+    tol = 8.0 * np.sqrt(V) * 2.0 ** -24 * 2.0 * np.abs(w).max() / N
+    assert ((du <= 1) | (np.abs(dh_g.astype(np.float64) - dh) <= tol)).all(), du.max()
+    assert (du <= 1).mean() >= 0.999 and (du == 0).mean() >= 0.98 and _rel(dh_g, dh) < 1e-3, \
+        ((du == 0).mean(), (du <= 1).mean(), _rel(dh_g, dh))
+    dw_g = ops.lm_wgrad_tx(dl, dlt, T_, H).cpu().numpy()
     assert _rel(dw_g, dw) < 1e-4, _rel(dw_g, dw)

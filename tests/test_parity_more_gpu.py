@@ -202,15 +202,16 @@ def test_loss_curve_20_steps_teacher_forced(ref):
 
 
 # ------------------------------------------------------------------ real widths
-def _update_flips(after, before, ref_after):
-    """Fraction of elements whose one-step update direction differs from the
-    reference's.  The first AdamW step is sign-like (m/sqrt(v) = g/|g|,
-    src/optim.cpp:61-70), so a last-bit gradient difference on an element whose
-    gradient is ~0 moves that element by a full 2*lr: updated params are
-    compared by how many directions flip, not norm-wise."""
+def _update_flips(after, before, ref_after, g_ref):
+    """Gradient mass whose one-step update direction differs from the
+    reference's: sum |g_ref| over flipped elements / sum |g_ref|.  The first
+    AdamW step is sign-like (m/sqrt(v) = g/|g|, src/optim.cpp:61-70), so a
+    last-bit difference in a gradient that is ~0 moves that element by a full
+    2*lr; weighting by |g| counts the flips of elements that carry gradient."""
     a = np.sign(np.asarray(after, np.float64) - before)
     b = np.sign(np.asarray(ref_after, np.float64) - before)
-    return float((a != b).mean())
+    w = np.abs(np.asarray(g_ref, np.float64))
+    return float(w[a != b].sum() / max(w.sum(), 1e-30))
 
 
 def _width_step(ref, preset, n_layers, T, seed=1234):
@@ -231,25 +232,27 @@ def _width_step(ref, preset, n_layers, T, seed=1234):
     lg, ng = sess.train_step(toks, 1, step=0)
     assert abs(lg - lw) / lw < 1e-3, (lg, lw)
     assert abs(ng - nw) / nw < 2e-2, (ng, nw)
-    # the reference with ONE E4M3 code step in one weight
-    pert = ref.RefModel(cfg.as_list(), seed, grad_e5m2=True)
-    w = pert.get("layers.0.w_qkv").copy()
-    i = int(np.argmax(np.abs(w) < 0.5 * np.abs(w).max()))
-    w[i] = ref.bf16_round(float(w[i]) * 1.125)
-    pert.set("layers.0.w_qkv", w)
-    pert.train_step(toks, 1, step=0)
+    # the reference with ONE E4M3 code step in one weight (two such perturbations, the
+    # envelope is the larger response)
+    perts = []
+    for tgt in ("layers.0.w_qkv", f"layers.{n_layers - 1}.w_down"):
+        pert = ref.RefModel(cfg.as_list(), seed, grad_e5m2=True)
+        w = pert.get(tgt).copy()
+        i = int(np.argmax(np.abs(w) < 0.5 * np.abs(w).max()))
+        w[i] = ref.bf16_round(float(w[i]) * 1.125)
+        pert.set(tgt, w)
+        pert.train_step(toks, 1, step=0)
+        perts.append((tgt, pert))
     worst = {}
     for n in rm.names:
         want_g = rm.acc_grad(n)
-        env_g = _rel(pert.acc_grad(n), want_g)
+        env_g = max(_rel(p.acc_grad(n), want_g) for _, p in perts)
         got_g = _rel(sess.grad(n), want_g)
         assert got_g <= max(2.0 * env_g, 5e-3), (n, "grad", got_g, env_g)
-        if n == "layers.0.w_qkv":
-            continue
-        env_f = _update_flips(pert.get(n), before[n], rm.get(n))
-        got_f = _update_flips(sess.download(n), before[n], rm.get(n))
+        env_f = max(_update_flips(p.get(n), before[n], rm.get(n), want_g) for t, p in perts if t != n)
+        got_f = _update_flips(sess.download(n), before[n], rm.get(n), want_g)
         worst[n] = (got_g, env_g, got_f, env_f)
-        assert got_f <= max(2.0 * env_f, 1e-3), (n, "update flips", got_f, env_f)
+        assert got_f <= max(2.0 * env_f, 5e-3), (n, "update flips", got_f, env_f)
     print({n: tuple(round(x, 5) for x in v) for n, v in worst.items()})
 
 

@@ -193,3 +193,27 @@ def test_session_footprint_and_session_search():
     assert res["feasible"], res
     for f in res["feasible"]:
         assert f["device_bytes"] <= hw.device_bytes
+
+
+def test_session_footprint_sharding_switches_save_memory():
+    """Qwen2.5-14B shape at W = 8 (BASELINE config 5): shard_weights keeps 1/8 of the bf16
+    block weights and streams the FP8 codes per layer; shard_grads reduce-scatters per layer
+    instead of holding the full gradient and receive buffers; offload.weights moves the
+    codes to pinned host memory.  Each switch lowers the session's real device arena."""
+    cfg = _cfg(PRESETS["14b"])
+    base = dict(mb=4, bf16_moments=True, lm=0, at=0)
+
+    def fp(**kw):
+        return PL.session_footprint(cfg, _plan(**{**base, **kw}), world=8)
+
+    d0, _ = fp()
+    d_sw, _ = fp(sw=True)
+    d_sg, _ = fp(sg=True)
+    d_both, _ = fp(sw=True, sg=True)
+    d_off, h_off = fp(sw=True, sg=True, ob=1 << 4)
+    gb = 1e9
+    assert d0 - d_sw > 30 * gb, (d0, d_sw)      # bf16 slices (23 GB) + codes (11 GB)
+    assert d0 - d_sg > 45 * gb, (d0, d_sg)      # gradients (25 GB) + receive buffer (25 GB)
+    assert d0 - d_both > 80 * gb, (d0, d_both)
+    assert d_off <= d_both and h_off > 13 * gb  # the host weight cache holds every layer's codes
+    assert d_both < 0.5 * d0, (d0 / gb, d_both / gb)
