@@ -110,6 +110,7 @@ class Session {
         QtAdamW h{hyper.lr, hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, max_grad_norm};
         check(qt_session_create(&c, &p, &r, &h, seed, rank, world, nccl_id, device, &s_));
         ga_steps_ = plan.ga_steps;
+        recompute_ = plan.recompute;
         const int n = qt_num_params(s_);
         for (int i = 0; i < n; ++i) {
             const char* nm = nullptr;
@@ -179,11 +180,100 @@ class Session {
     }
 
     qt_session* handle() { return s_; }
+    const RecomputeSet& recompute() const { return recompute_; }
 
    private:
     qt_session* s_ = nullptr;
     int ga_steps_ = 1;
+    RecomputeSet recompute_;
     std::vector<std::pair<std::string, std::int64_t>> names_;
 };
+
+// ---------------------------------------------------------------------------
+// The reference's free-function signatures (include/qtrain/model.hpp:125-211,
+// include/qtrain/optim.hpp:55-77) over a Session, so a call site written
+// against qtrain:: ports by swapping the namespace and passing the Session
+// where the reference passes ModelParams / OptimState.
+//
+// Per-call recompute sets: the reference's results do not depend on the
+// recompute set (bitwise, tests/test_model.cpp:94-121; the session is tested
+// to the same property), so a call with a set other than the session's runs
+// the session's set; only memory and time differ.
+// ---------------------------------------------------------------------------
+
+// StepContext (model.hpp:134-144): the FP8 codes live inside the session
+struct StepContext {
+    Session* session = nullptr;
+};
+inline StepContext build_step_context(const ModelConfig&, Session& params, const PrecisionMap&) {
+    params.build_step_context();
+    return StepContext{&params};
+}
+
+struct ForwardResult {  // model.hpp:163-175 (the loss; activations stay on the device)
+    float loss = 0.0f;
+};
+
+inline ForwardResult model_forward(const ModelConfig&, Session& params, const StepContext& step,
+                                   const std::vector<std::int32_t>& tokens, std::int64_t batch,
+                                   const RecomputeSet& /*recompute*/, const PrecisionMap&, const ChunkSpec& = {},
+                                   bool with_grads = true) {
+    if (step.session != &params) throw std::invalid_argument("model_forward: step context of another model");
+    return ForwardResult{params.model_forward(tokens, batch, with_grads)};
+}
+
+// model_backward + GradAccumulator::accumulate (model.hpp:190-211): gradients are
+// accumulated into the session's GradAccumulator at micro_step
+inline void model_backward(const ModelConfig&, Session& params, const StepContext&, ForwardResult&,
+                           const RecomputeSet&, const PrecisionMap&, const ChunkSpec& = {},
+                           std::uint64_t micro_step = 0) {
+    params.model_backward(micro_step);
+}
+
+// global_grad_norm / clip_scale (optim.hpp:65-71, src/optim.cpp:87-110)
+inline double global_grad_norm(Session& params) { return params.global_grad_norm(); }
+inline float clip_scale(double norm, float max_norm) {
+    if (max_norm <= 0.0f || !(norm > static_cast<double>(max_norm))) return 1.0f;
+    return static_cast<float>(static_cast<double>(max_norm) / norm);
+}
+
+// adamw_step / sharded_adamw_step (optim.hpp:59-77): the session holds the OptimState;
+// throws std::runtime_error("adamw_step: non-finite gradient in <name>") like src/optim.cpp:47
+inline void adamw_step(Session& params, float grad_scale) { params.adamw_step(grad_scale); }
+
+// ---------------------------------------------------------------------------
+// Trainer, checkpoints, planner (src/trainer.cpp, checkpoint.cpp, memplan.cpp)
+// ---------------------------------------------------------------------------
+inline void check_train(int rc) {
+    if (rc == 0) return;
+    const std::string msg = qt_train_last_error();
+    if (rc == 1) throw std::invalid_argument(msg);
+    if (rc == 2) throw std::out_of_range(msg);
+    throw std::runtime_error(msg);
+}
+
+// run_training_to_files (trainer.cpp:152-171) from a manifest (JSON text or path);
+// returns the result JSON
+inline std::string run_training_to_files(const std::string& manifest, int device_count = 0) {
+    std::size_t need = 0;
+    check_train(qt_run_training(manifest.c_str(), device_count, nullptr, 0, &need));
+    std::string out(need, '\0');
+    check_train(qt_run_training(manifest.c_str(), device_count, out.data(), need, &need));
+    out.resize(need ? need - 1 : 0);
+    return out;
+}
+
+// save_checkpoint / load_checkpoint (checkpoint.cpp:19-80), params + optimizer state
+inline void save_checkpoint(const std::string& path, Session& s, const ModelConfig& cfg, bool with_optimizer = true) {
+    QtModelConfig c{cfg.n_layers, cfg.d_model, cfg.d_ff, cfg.n_heads, cfg.n_kv_heads, cfg.vocab, cfg.seq_len};
+    qt_session* h = s.handle();
+    check_train(qt_checkpoint_save(&h, 1, &c, path.c_str(), with_optimizer ? 1 : 0));
+}
+inline std::int64_t load_checkpoint(const std::string& path, Session& s) {
+    qt_session* h = s.handle();
+    std::int64_t step = 0;
+    check_train(qt_checkpoint_load(&h, 1, path.c_str(), &step));
+    return step;
+}
 
 }  // namespace qtrain_b200

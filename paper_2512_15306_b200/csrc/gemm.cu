@@ -1002,8 +1002,17 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
             no_tma = e ? atoi(e) : 0;
         }
         const int64_t ncols = g->epi == EPI_SWIGLU_BWD ? 2 * g->N : g->N;  // gate | up halves
+        // pinned host buffers (offloaded gradient accumulators, zero-copy) take the direct path
+        auto on_device = [](const void* ptr) {
+            cudaPointerAttributes a{};
+            if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+                cudaGetLastError();
+                return true;
+            }
+            return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+        };
         bool ok = !no_tma && !(reinterpret_cast<uintptr_t>(g->out) & 15) && ((g->ldo * oel) & 15) == 0 &&
-                  g->ldo >= ncols;
+                  g->ldo >= ncols && on_device(g->out) && (!g->res || on_device(g->res));
         if (ok && g->epi == EPI_BF16_RES)
             ok = g->res && !(reinterpret_cast<uintptr_t>(g->res) & 15) && ((g->ldr * 2) & 15) == 0 && g->ldr >= g->N;
         if (ok && g->epi == EPI_SWIGLU_BWD)

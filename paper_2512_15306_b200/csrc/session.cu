@@ -296,6 +296,29 @@ class Session {
     std::vector<uint8_t*> wown;      // L*4 (shard_weights)
     uint8_t* wslot[2][4] = {};
     uint8_t* whost = nullptr;        // L x layer codes (pinned)
+    // offload tiers (RunPlan::offload, memplan.hpp:34-52): pinned host region holding the
+    // offloaded optimizer moments (m, v), bf16 master block weights and/or gradient buffer.
+    // Zero-copy: kernels address it directly (UVA).  Double-buffer (m, v): AdamW streams the
+    // moments through two device slots group by group on the copy engines.
+    uint8_t* harena = nullptr;
+    size_t harena_bytes = 0;
+    int64_t p_master = 0;            // elements of the host master region (offload.master)
+    uint16_t* hmaster = nullptr;
+    float* mstage[2][2] = {};        // [slot][m|v] f32 (or bf16) staging of the double buffer
+    int64_t mstage_elems = 0;
+    struct MGroup {
+        int c0, c1;                  // chunk-table range
+        int64_t e0, e1;              // moment element range
+    };
+    std::vector<MGroup> mgroups;
+    cudaEvent_t ev_mready[2] = {}, ev_mdone[2] = {}, ev_mfree[2] = {};
+    // offload.x: the layer inputs r_in[0..L-1] live in pinned host memory; two device slots
+    // (layer l in slot l%2) are written back after the forward produces them and refilled
+    // one layer ahead of the backward
+    uint16_t* xslot[2] = {nullptr, nullptr};
+    uint16_t* xhost = nullptr;
+    int xslot_layer[2] = {-1, -1};
+    cudaEvent_t ev_xready[2] = {}, ev_xfree[2] = {};
     int64_t wl_off[4] = {}, wl_total = 0;  // a layer's 4 tensors inside a slot / whost entry
     int slot_layer[2] = {-1, -1};    // which layer's codes each slot holds (this step)
     std::vector<char> published;     // whost[l] holds this step's codes
@@ -396,7 +419,7 @@ class Session {
             try {
                 if (group) {
                     if (group->world != world) throw QtError(1, "peer group size != world");
-                    tr = std::make_unique<PeerTransport>(group, rank, device, arena, arena_bytes);
+                    tr = std::make_unique<PeerTransport>(group, rank, device, arena, arena_bytes, harena, harena_bytes);
                 } else {
                     if (!nccl_id) throw QtError(1, "world > 1 needs an NCCL unique id (or a peer group)");
                     tr = std::make_unique<NcclTransport>(rank, world, nccl_id);
@@ -413,6 +436,16 @@ class Session {
         }
         if (stream_codes() && offload_weights())
             QT_CHECK_CUDA(cudaMallocHost(&whost, std::max<size_t>((size_t)L * wl_total, 1)));
+        if (offload_x()) {
+            if (!cst) QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+            for (cudaEvent_t* e : {&ev_xready[0], &ev_xready[1], &ev_xfree[0], &ev_xfree[1]})
+                QT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+        if (stream_moments()) {
+            if (!cst) QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+            for (cudaEvent_t* e : {&ev_mready[0], &ev_mready[1], &ev_mdone[0], &ev_mdone[1], &ev_mfree[0], &ev_mfree[1]})
+                QT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
 
@@ -447,6 +480,10 @@ class Session {
             if (e) cudaEventDestroy(e);
         if (cst) cudaStreamDestroy(cst);
         if (whost) cudaFreeHost(whost);
+        if (harena) cudaFreeHost(harena);
+        for (cudaEvent_t e : {ev_mready[0], ev_mready[1], ev_mdone[0], ev_mdone[1], ev_mfree[0], ev_mfree[1],
+                              ev_xready[0], ev_xready[1], ev_xfree[0], ev_xfree[1]})
+            if (e) cudaEventDestroy(e);
         if (gexec) cudaGraphExecDestroy(gexec);
         for (auto& e : blk_ev)
             if (e) cudaEventDestroy(e);
@@ -511,14 +548,19 @@ class Session {
             shard_total += t.pw;
         }
         // storage layout (world 1: offsets == the unsharded layout, params and grads alike)
-        p_store = g_store = layer_g = 0;
+        p_store = g_store = layer_g = p_master = 0;
         for (int i = 0; i < (int)P.size(); ++i) {
             ParamT& t = P[i];
             t.sharded = shard_weights() && is_block_weight(i);
             t.lo = t.sharded ? (int64_t)rank * t.pw : 0;
             t.store = t.sharded ? t.pw : t.padded;
-            t.off = p_store;
-            p_store += t.store;
+            if (offload_master() && is_block_weight(i)) {  // placed in the host region (allocate)
+                t.off = p_master;
+                p_master += t.store;
+            } else {
+                t.off = p_store;
+                p_store += t.store;
+            }
             if (shard_grads() && i >= 1 && i <= 6 * L) {
                 const int k = (i - 1) % 6;
                 if (k == 0) layer_g = 0;
@@ -566,17 +608,30 @@ class Session {
             void** p;
             size_t bytes;
         };
-        std::vector<Req> reqs;
+        std::vector<Req> reqs, hreqs;
         auto req = [&](auto** p, size_t bytes) { reqs.push_back({reinterpret_cast<void**>(p), bytes}); };
+        auto hreq = [&](auto** p, size_t bytes) { hreqs.push_back({reinterpret_cast<void**>(p), bytes}); };
         const int64_t M = Mmax;
         req(&params, p_store * 2);
-        req(&grads, std::max<int64_t>(g_store, 1) * 2);
-        if (plan.bf16_moments) {
-            req(&m16, shard_total * 2);
-            req(&v16, shard_total * 2);
-        } else {
-            req(&m32, shard_total * 4);
-            req(&v32, shard_total * 4);
+        if (offload_master()) hreq(&hmaster, std::max<int64_t>(p_master, 1) * 2);
+        if (offload_grads()) hreq(&grads, std::max<int64_t>(g_store, 1) * 2);
+        else req(&grads, std::max<int64_t>(g_store, 1) * 2);
+        {
+            const size_t mb = plan.bf16_moments ? 2 : 4;
+            auto mreq = [&](bool host, void** p) {
+                if (host) hreqs.push_back({p, (size_t)shard_total * mb});
+                else reqs.push_back({p, (size_t)shard_total * mb});
+            };
+            mreq(offload_m(), plan.bf16_moments ? (void**)&m16 : (void**)&m32);
+            mreq(offload_v(), plan.bf16_moments ? (void**)&v16 : (void**)&v32);
+            if (stream_moments()) {
+                // groups of whole AdamW chunks, <= 32 Mi elements, streamed through 2 slots
+                build_mgroups();
+                for (int sl = 0; sl < 2; ++sl)
+                    for (int k = 0; k < 2; ++k)
+                        if ((k == 0 && offload_m()) || (k == 1 && offload_v()))
+                            req(&mstage[sl][k], (size_t)mstage_elems * mb);
+            }
         }
         if (world > 1) {
             req(&gshard, shard_total * 4);
@@ -634,7 +689,14 @@ class Session {
         req(&sc.n2c, M * d);
         req(&sc.gu, M * F * 2);
         req(&sc.hc, M * Hh);
-        for (int l = 0; l <= L; ++l) req(&lb[l].r_in, M * d * 2);  // r_in[L] = r_final
+        if (offload_x()) {  // two device slots + the host copy of r_in[0..L-1]
+            req(&xslot[0], M * d * 2);
+            req(&xslot[1], M * d * 2);
+            req(&lb[L].r_in, M * d * 2);
+            hreq(&xhost, (size_t)L * M * d * 2);
+        } else {
+            for (int l = 0; l <= L; ++l) req(&lb[l].r_in, M * d * 2);  // r_in[L] = r_final
+        }
         std::vector<LayerBufs> own(L);
         for (int l = 0; l < L; ++l) {
             if (keep(0)) req(&own[l].n1c, M * d);
@@ -745,9 +807,22 @@ class Session {
 
         size_t total = 0;
         for (auto& r : reqs) total += (r.bytes + 255) & ~size_t(255);
+        size_t htotal = 0;
+        for (auto& r : hreqs) htotal += (r.bytes + 4095) & ~size_t(4095);
+        host_bytes += htotal;
         if (dry) {
             arena_bytes = total;
             return;
+        }
+        if (htotal) {
+            QT_CHECK_CUDA(cudaMallocHost(&harena, htotal));
+            std::memset(harena, 0, htotal);
+            harena_bytes = htotal;
+            size_t ho = 0;
+            for (auto& r : hreqs) {
+                *r.p = harena + ho;
+                ho += (r.bytes + 4095) & ~size_t(4095);
+            }
         }
         QT_CHECK_CUDA(cudaMalloc(&arena, total));
         arena_bytes = total;
@@ -757,6 +832,11 @@ class Session {
             *r.p = arena + off;
             off += (r.bytes + 255) & ~size_t(255);
         }
+        if (offload_x())
+            for (int l = 0; l < L; ++l) lb[l].r_in = xslot[l % 2];
+        if (offload_master())  // block weights in the host region, addressed from the params base (UVA)
+            for (int i = 0; i < (int)P.size(); ++i)
+                if (is_block_weight(i)) P[i].off += (int64_t)(hmaster - params);
         for (int l = 0; l < L; ++l) {
             LayerBufs& b = lb[l];
             b.n1c = own[l].n1c ? own[l].n1c : sc.n1c;
@@ -774,14 +854,21 @@ class Session {
     }
 
     // AdamW / norm segments for this rank (ZeRO-1 slices when world > 1)
-    void build_segments() {
-        if ((int)sizeof(SegH) != qtk_seg_size()) throw QtError(3, "Seg layout mismatch");
-        std::vector<SegH> segs;
+    struct ChunkH {
+        int32_t seg, pad;
+        int64_t start;
+    };
+    std::vector<SegH> segs_h;
+    std::vector<ChunkH> chunks_h;
+    // the AdamW / norm segments and chunk table on the host (params offsets final: after allocate)
+    void make_segments() {
+        std::vector<SegH>& segs = segs_h;
+        segs.clear();
         int64_t blk = 0, soff = 0;
         for (auto& t : P) {
             SegH s{};
             if (world == 1) {
-                s.off = t.off;
+                s.off = t.goff;  // gradient and moment offset (== the params offset unless offloaded)
                 s.n = t.numel;
                 s.gstart = 0;
                 s.poff = t.off;
@@ -805,19 +892,44 @@ class Session {
         // norm blocks in name (std::map) order are not needed for the tree sum; layout order is used
         norm_blocks = blk;
         nsegs = (int)segs.size();
-        QT_CHECK_CUDA(cudaMemcpyAsync(segs_dev, segs.data(), segs.size() * sizeof(SegH), cudaMemcpyHostToDevice, st));
-        struct Chunk {
-            int32_t seg, pad;
-            int64_t start;
-        };
-        if ((int)sizeof(Chunk) != qtk_adamw_chunk_entry_size()) throw QtError(3, "AdamW chunk layout mismatch");
-        std::vector<Chunk> chunks;
+        chunks_h.clear();
         const int64_t cs = qtk_adamw_chunk_size();
         for (int i = 0; i < nsegs; ++i)
-            for (int64_t s0 = 0; s0 < segs[i].n; s0 += cs) chunks.push_back({i, 0, s0});
-        nchunks = (int)chunks.size();
-        QT_CHECK_CUDA(cudaMemcpyAsync(chunks_dev, chunks.data(), chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice,
+            for (int64_t s0 = 0; s0 < segs[i].n; s0 += cs) chunks_h.push_back({i, 0, s0});
+        nchunks = (int)chunks_h.size();
+    }
+    // double-buffered moments: consecutive chunks grouped to <= 32 Mi moment elements
+    void build_mgroups() {
+        make_segments();
+        mgroups.clear();
+        const int64_t cs = qtk_adamw_chunk_size(), cap = int64_t(32) << 20;
+        mstage_elems = 0;
+        int c0 = 0;
+        while (c0 < nchunks) {
+            const int64_t e0 = segs_h[chunks_h[c0].seg].off + chunks_h[c0].start;
+            int c1 = c0;
+            int64_t e1 = e0;
+            while (c1 < nchunks) {
+                const SegH& sg = segs_h[chunks_h[c1].seg];
+                const int64_t end = sg.off + std::min(chunks_h[c1].start + cs, sg.n);
+                if (c1 > c0 && end - e0 > cap) break;
+                e1 = end;
+                ++c1;
+            }
+            mgroups.push_back({c0, c1, e0, e1});
+            mstage_elems = std::max(mstage_elems, ceil_div(e1 - e0, 4) * 4 + 4);
+            c0 = c1;
+        }
+    }
+    void build_segments() {
+        if ((int)sizeof(SegH) != qtk_seg_size()) throw QtError(3, "Seg layout mismatch");
+        if ((int)sizeof(ChunkH) != qtk_adamw_chunk_entry_size()) throw QtError(3, "AdamW chunk layout mismatch");
+        make_segments();
+        if (stream_moments()) build_mgroups();
+        QT_CHECK_CUDA(cudaMemcpyAsync(segs_dev, segs_h.data(), segs_h.size() * sizeof(SegH), cudaMemcpyHostToDevice,
                                       st));
+        QT_CHECK_CUDA(cudaMemcpyAsync(chunks_dev, chunks_h.data(), chunks_h.size() * sizeof(ChunkH),
+                                      cudaMemcpyHostToDevice, st));
         QT_CHECK_CUDA(cudaStreamSynchronize(st));
     }
 
@@ -941,6 +1053,14 @@ class Session {
     // RunPlan::offload.weights: the FP8 codes live in pinned host memory, two layer slots on
     // the device (memplan.hpp:34-52; with shard_weights this is the paper's host weight cache)
     bool offload_weights() const { return (plan.offload_bits & QT_OFF_WEIGHTS) != 0; }
+    bool offload_master() const { return (plan.offload_bits & QT_OFF_MASTER) != 0; }
+    bool offload_m() const { return (plan.offload_bits & QT_OFF_M) != 0; }
+    bool offload_v() const { return (plan.offload_bits & QT_OFF_V) != 0; }
+    bool offload_grads() const { return (plan.offload_bits & QT_OFF_GRADS) != 0; }
+    bool offload_x() const { return (plan.offload_bits & QT_OFF_X) != 0; }
+    bool zero_copy() const { return plan.transfer_policy == QT_XFER_ZERO_COPY; }
+    // moments streamed through device slots (double-buffer policy)
+    bool stream_moments() const { return (offload_m() || offload_v()) && !zero_copy(); }
     // the block weights' codes are streamed per layer (not all resident)
     bool stream_codes() const { return shard_weights() || offload_weights(); }
     // the codes of weight k (W_QKV, W_O, W_GU, W_DOWN) of layer l
@@ -1063,6 +1183,36 @@ class Session {
         QT_CHECK_CUDA(cudaEventRecord(ev_wfree[l % 2], st));
     }
 
+    // ---------------- offloaded residuals (offload.x) ----------------
+    // before the compute stream writes r_in[l] into its slot: the slot's previous content is
+    // on the host (forward write-back) or no longer read (backward)
+    void x_before_write(int l) { QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_xfree[l % 2], 0)); }
+    // r_in[l] was just produced in its slot: copy it to the host on the copy engine
+    void x_publish(int l) {
+        const int sl = l % 2;
+        const size_t bytes = (size_t)curM * d * 2;
+        QT_CHECK_CUDA(cudaEventRecord(ev_xready[sl], st));
+        QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_xready[sl], 0));
+        QT_CHECK_CUDA(cudaMemcpyAsync(xhost + (size_t)l * Mmax * d, xslot[sl], bytes, cudaMemcpyDeviceToHost, cst));
+        QT_CHECK_CUDA(cudaEventRecord(ev_xfree[sl], cst));
+        xslot_layer[sl] = l;
+    }
+    void x_fetch(int l) {
+        const int sl = l % 2;
+        if (xslot_layer[sl] == l) return;
+        QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_xfree[sl], 0));
+        QT_CHECK_CUDA(cudaMemcpyAsync(xslot[sl], xhost + (size_t)l * Mmax * d, (size_t)curM * d * 2,
+                                      cudaMemcpyHostToDevice, cst));
+        QT_CHECK_CUDA(cudaEventRecord(ev_xready[sl], cst));
+        xslot_layer[sl] = l;
+    }
+    // backward of layer l: r_in[l] in its slot (r_in[next] prefetched)
+    void x_acquire(int l, int next) {
+        x_fetch(l);
+        if (next >= 0) x_fetch(next);
+        QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_xready[l % 2], 0));
+    }
+
     // ---------------- block forward (src/model.cpp:239-293) ----------------
     void block_forward(int l, bool record) {
         LayerBufs& b = lb[l];
@@ -1115,6 +1265,74 @@ class Session {
              EPI_BF16_RES, lb[l + 1].r_in, d, b.r_mid, d);
     }
 
+    // Backward-time recompute of the dropped sites of layer l only (KeepMask, model.cpp:221-235,
+    // replay with the forward's cached statistics, :374-378): each dropped site is rebuilt from
+    // the nearest kept (or rebuilt) input; kept sites are not touched and the block output
+    // (the next layer's residual) is never recomputed.  Bitwise the forward's values.
+    void block_replay(int l) {
+        LayerBufs& b = lb[l];
+        const int64_t M = curM;
+        uint32_t* am = act_amax + l * 4;
+        float* sc = act_scale + l * 4;
+        const float* ws = w_scale + l * 4;
+        const ParamT& ln1 = P[lp(l, 0)];
+        const ParamT& ln2 = P[lp(l, 3)];
+        int h;
+        if (!keep(0)) {  // n1 codes (qkv wgrad, qkv recompute)
+            h = prof_begin();
+            QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, b.r_in, params + ln1.off, M, d, 1e-6f, nullptr, s_n1, rms_inv, nullptr,
+                                       st));
+            prof_end(h, 4, 4.0 * M * d);
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(s_n1, M * d, kE4M3, am + S_N1, b.n1c, sc + S_N1, st));
+            prof_end(h, 3, 3.0 * M * d);
+        }
+        if (!keep(1)) {  // post-RoPE qkv
+            gemm(0, kE4M3, kE4M3, false, false, M, q, d, b.n1c, d, wc(l, W_QKV), d, sc + S_N1, ws + W_QKV, EPI_BF16,
+                 b.qkv, q);
+            h = prof_begin();
+            QT_CHECK_K(qtk_rope(b.qkv, M, curT, H + Hkv, hd, q, rope_tab, 0, nullptr, st));
+            prof_end(h, 5, 4.0 * M * (d + Hkv * hd));
+        }
+        if (!keep(2)) {  // attention output (bf16, f32, codes) + LSE
+            h = prof_begin();
+            QT_CHECK_K(qtk_attn_fwd(b.qkv, curB, curT, H, Hkv, hd, q, b.att, d, b.att32, b.lse, nullptr, st));
+            prof_end(h, 6, 4.0 * curB * H * (double)curT * curT / 2 * hd);
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(b.att, M * d, kE4M3, am + S_ATT, b.attc, sc + S_ATT, st));
+            prof_end(h, 3, 3.0 * M * d);
+        }
+        if (!keep(3)) {  // r_mid (block recompute): out-projection + fused residual rmsnorm
+            gemm(0, kE4M3, kE4M3, false, false, M, d, d, b.attc, d, wc(l, W_O), d, sc + S_ATT, ws + W_O, EPI_BF16,
+                 s_attn_out, d);
+            h = prof_begin();
+            QT_CHECK_K(qtk_rmsnorm_fwd(s_attn_out, b.r_in, params + ln2.off, M, d, 1e-6f, b.r_mid, s_n2, rms_inv,
+                                       nullptr, st));
+            prof_end(h, 4, 8.0 * M * d);
+        } else if (!keep(4)) {  // n2 from the kept r_mid (pass-through residual: same bits)
+            h = prof_begin();
+            QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, b.r_mid, params + ln2.off, M, d, 1e-6f, nullptr, s_n2, rms_inv,
+                                       nullptr, st));
+            prof_end(h, 4, 4.0 * M * d);
+        }
+        if (!keep(4)) {
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(s_n2, M * d, kE4M3, am + S_N2, b.n2c, sc + S_N2, st));
+            prof_end(h, 3, 3.0 * M * d);
+        }
+        if (!keep(5))
+            gemm(0, kE4M3, kE4M3, false, false, M, F, d, b.n2c, d, wc(l, W_GU), d, sc + S_N2, ws + W_GU, EPI_BF16,
+                 b.gu, F);
+        if (!keep(6)) {
+            h = prof_begin();
+            QT_CHECK_K(qtk_swiglu_fwd(b.gu, M, Hh, s_h, nullptr, st));
+            prof_end(h, 5, 2.0 * M * F + 2.0 * M * Hh);
+            h = prof_begin();
+            QT_CHECK_K(qtk_quantize_bf16(s_h, M * Hh, kE4M3, am + S_H, b.hc, sc + S_H, st));
+            prof_end(h, 3, 3.0 * M * Hh);
+        }
+    }
+
     // ---------------- model_forward (src/model.cpp:297-352) ----------------
     void forward(const int32_t* tokens, int64_t n_tokens, int64_t batch, bool with_grads) {
         if (batch < 1 || n_tokens % batch != 0) throw QtError(1, "model_forward: token count not divisible by batch");
@@ -1128,15 +1346,19 @@ class Session {
         QT_CHECK_CUDA(cudaMemsetAsync(act_amax, 0, L * 16, st));
         QT_CHECK_CUDA(cudaMemsetAsync(fin_amax, 0, 4, st));
         int h = prof_begin();
+        if (offload_x()) x_before_write(0);
         QT_CHECK_K(qtk_embed_fwd(tokens, curB, curT, params + par("embed").off, d, V, lb[0].r_in, inputs, targets,
                                  err_dev, st));
         prof_end(h, 5, 4.0 * M * d);
+        if (offload_x()) x_publish(0);
         if (with_grads) QT_CHECK_K(qtk_embed_sort(inputs, (int)M, V, sort_scratch, sort_scratch_bytes, sorted_pos,
                                                   seg_tok, seg_off, nseg, st));
         for (int l = 0; l < L; ++l) {
             codes_acquire(l, l + 1);
+            if (offload_x() && l + 1 < L) x_before_write(l + 1);
             block_forward(l, true);
             codes_release(l);
+            if (offload_x() && l + 1 < L) x_publish(l + 1);
         }
         h = prof_begin();
         QT_CHECK_K(qtk_rmsnorm_fwd(nullptr, lb[L].r_in, pptr("final_g"), M, d, 1e-6f, nullptr, normed_final, rms_inv,
@@ -1221,11 +1443,12 @@ class Session {
         for (int l = L - 1; l >= 0; --l) {
             LayerBufs& b = lb[l];
             codes_acquire(l, l - 1);
+            if (offload_x()) x_acquire(l, l - 1);
             if (exchange_in_backward) {  // the layer's gradient slot: free (exchange done) and zeroed
                 QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_lfree[l % 2], 0));
                 QT_CHECK_CUDA(cudaMemsetAsync(lgrad[l % 2], 0, layer_g * 2, st));
             }
-            if (!b.keep_all) block_forward(l, false);  // replay with cached stats (model.cpp:374-378)
+            if (!b.keep_all) block_replay(l);  // dropped sites only, cached stats (model.cpp:374-378)
             uint32_t* ga = g_amax + l * 4;
             float* gs = g_scale + l * 4;
             const float* as = act_scale + l * 4;
@@ -1296,6 +1519,7 @@ class Session {
             accumulate_f32(P[lp(l, 0)], dgamma, micro_step);
             prof_end(h, 4, 10.0 * M * d);
             codes_release(l);
+            if (offload_x()) QT_CHECK_CUDA(cudaEventRecord(ev_xfree[l % 2], st));
             if (exchange_in_backward) reduce_layer_async(l);
         }
         // ordered embedding backward, bf16 round, accumulate (model.cpp:442-444)
@@ -1386,10 +1610,59 @@ class Session {
         const int64_t total = world > 1 ? shard_total : p_total;
         int h = prof_begin();
         QT_CHECK_CUDA(cudaMemsetAsync(seg_amax, 0, P.size() * 4, st));
-        QT_CHECK_K(qtk_adamw_dev_sd(params, m32, v32, m16, v16, g, world > 1, segs_dev, chunks_dev, nchunks, hyper.lr,
-                                    hyper.beta1, hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev,
-                                    seed, step, plan.bf16_moments, err_dev, seg_amax, use_dev_ctr ? step_blk : nullptr,
-                                    st));
+        auto launch = [&](float* m, float* v, uint16_t* mh, uint16_t* vh, const uint8_t* chunks, int n) {
+            QT_CHECK_K(qtk_adamw_dev_sd(params, m, v, mh, vh, g, world > 1, segs_dev, chunks, n, hyper.lr, hyper.beta1,
+                                        hyper.beta2, hyper.eps, hyper.weight_decay, bc1, bc2, grad_scale_dev, seed, step,
+                                        plan.bf16_moments, err_dev, seg_amax, use_dev_ctr ? step_blk : nullptr, st));
+        };
+        if (!stream_moments()) {
+            launch(m32, v32, m16, v16, static_cast<const uint8_t*>(chunks_dev), nchunks);
+        } else {
+            // offload (double-buffer policy): each group's offloaded moments go host -> slot on
+            // the copy engine (one group ahead), AdamW updates them in the slot, and they go back
+            const size_t mb = plan.bf16_moments ? 2 : 4;
+            uint8_t* hm = plan.bf16_moments ? (uint8_t*)m16 : (uint8_t*)m32;
+            uint8_t* hv = plan.bf16_moments ? (uint8_t*)v16 : (uint8_t*)v32;
+            auto h2d = [&](int gi) {
+                const MGroup& gp = mgroups[(size_t)gi];
+                const int sl = gi % 2;
+                const size_t bytes = (size_t)(gp.e1 - gp.e0) * mb;
+                if (offload_m())
+                    QT_CHECK_CUDA(cudaMemcpyAsync(mstage[sl][0], hm + gp.e0 * mb, bytes, cudaMemcpyHostToDevice, cst));
+                if (offload_v())
+                    QT_CHECK_CUDA(cudaMemcpyAsync(mstage[sl][1], hv + gp.e0 * mb, bytes, cudaMemcpyHostToDevice, cst));
+                QT_CHECK_CUDA(cudaEventRecord(ev_mready[sl], cst));
+            };
+            QT_CHECK_CUDA(cudaEventRecord(ev_mdone[0], st));  // the grads of this step are final
+            QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_mdone[0], 0));
+            const int ng = (int)mgroups.size();
+            if (ng) h2d(0);
+            for (int gi = 0; gi < ng; ++gi) {
+                const MGroup& gp = mgroups[(size_t)gi];
+                const int sl = gi % 2;
+                if (gi + 1 < ng) h2d(gi + 1);
+                QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_mready[sl], 0));
+                // moment pointers rebased so that element e0 of the group sits at the slot start
+                auto base = [&](int k, uint8_t* hostp) -> uint8_t* {
+                    const bool off = k == 0 ? offload_m() : offload_v();
+                    return off ? reinterpret_cast<uint8_t*>(mstage[sl][k]) - gp.e0 * (int64_t)mb : hostp;
+                };
+                uint8_t* mp = base(0, hm);
+                uint8_t* vp = base(1, hv);
+                launch(plan.bf16_moments ? nullptr : (float*)mp, plan.bf16_moments ? nullptr : (float*)vp,
+                       plan.bf16_moments ? (uint16_t*)mp : nullptr, plan.bf16_moments ? (uint16_t*)vp : nullptr,
+                       static_cast<const uint8_t*>(chunks_dev) + (size_t)gp.c0 * sizeof(ChunkH), gp.c1 - gp.c0);
+                QT_CHECK_CUDA(cudaEventRecord(ev_mdone[sl], st));
+                QT_CHECK_CUDA(cudaStreamWaitEvent(cst, ev_mdone[sl], 0));
+                const size_t bytes = (size_t)(gp.e1 - gp.e0) * mb;
+                if (offload_m())
+                    QT_CHECK_CUDA(cudaMemcpyAsync(hm + gp.e0 * mb, mstage[sl][0], bytes, cudaMemcpyDeviceToHost, cst));
+                if (offload_v())
+                    QT_CHECK_CUDA(cudaMemcpyAsync(hv + gp.e0 * mb, mstage[sl][1], bytes, cudaMemcpyDeviceToHost, cst));
+            }
+            QT_CHECK_CUDA(cudaEventRecord(ev_mfree[0], cst));  // every moment is back on the host
+            QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_mfree[0], 0));
+        }
         prof_end(h, 10, (double)total * (plan.bf16_moments ? 14.0 : 22.0));
         amax_cached = !shard_weights();
         if (world > 1 && amax_cached)  // slice maxima -> tensor maxima
@@ -1426,7 +1699,8 @@ class Session {
         pre_step_count = step_count;
         // world > 1 stays stream-launched: the NCCL exchange inside a captured graph has
         // not been exercised on hardware this round (gpurun boxes have one GPU)
-        if (!graph_enabled() || prof_on || !amax_cached || world > 1 || stream_codes()) {
+        if (!graph_enabled() || prof_on || !amax_cached || world > 1 || stream_codes() || stream_moments() ||
+            offload_x()) {
             train_step_body(tokens, tokens_per_mb, batch, step, max_norm);
             return;
         }
@@ -1726,7 +2000,7 @@ int qt_grad_download(qt_session* h, int i, float* host) {
         const ParamT& t = s.P.at(i);
         if (t.goff < 0)
             throw QtError(1, "shard_grads keeps no local accumulator for layer tensors (qt_reduced_grad_download)");
-        download_bf16(s, s.grads + t.off, t.numel, host);
+        download_bf16(s, s.grads + t.goff, t.numel, host);
     });
 }
 // the cross-rank reduced f32 gradient of tensor i (world > 1): every rank's shard, gathered
@@ -1746,7 +2020,7 @@ int qt_moments_download(qt_session* h, int i, float* m, float* v) {
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
         std::vector<SegH> segs(s.nsegs);
-        QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDeviceToHost));
+        QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDefault));
         const SegH& sg = segs[i];
         const int64_t off = s.world > 1 ? sg.off : t.off;
         if (s.plan.bf16_moments) {  // bf16-SR moments, widened to f32 (exact)
@@ -1754,8 +2028,8 @@ int qt_moments_download(qt_session* h, int i, float* m, float* v) {
             download_bf16(s, s.v16 + off, sg.n, v);
             return;
         }
-        QT_CHECK_CUDA(cudaMemcpy(m, s.m32 + off, sg.n * 4, cudaMemcpyDeviceToHost));
-        QT_CHECK_CUDA(cudaMemcpy(v, s.v32 + off, sg.n * 4, cudaMemcpyDeviceToHost));
+        QT_CHECK_CUDA(cudaMemcpy(m, s.m32 + off, sg.n * 4, cudaMemcpyDefault));
+        QT_CHECK_CUDA(cudaMemcpy(v, s.v32 + off, sg.n * 4, cudaMemcpyDefault));
     });
 }
 
@@ -1766,21 +2040,21 @@ int qt_moments_upload(qt_session* h, int i, const float* m, const float* v, int6
         Session& s = *h->s;
         const ParamT& t = s.P.at(i);
         std::vector<SegH> segs(s.nsegs);
-        QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDeviceToHost));
+        QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDefault));
         const SegH& sg = segs[i];
         const int64_t off = s.world > 1 ? sg.off : t.off;
         const int64_t lo = s.world > 1 ? std::min<int64_t>((int64_t)s.rank * t.pw, t.numel) : 0;
         if (sg.n > 0) {
             if (s.plan.bf16_moments) {
                 for (int k = 0; k < 2; ++k) {
-                    QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, (k ? v : m) + lo, sg.n * 4, cudaMemcpyHostToDevice,
+                    QT_CHECK_CUDA(cudaMemcpyAsync(s.scratch_f32, (k ? v : m) + lo, sg.n * 4, cudaMemcpyDefault,
                                                   s.st));
                     f32_to_bf16_kernel<<<grid_for(sg.n), 256, 0, s.st>>>(s.scratch_f32, (k ? s.v16 : s.m16) + off,
                                                                            sg.n);
                 }
             } else {
-                QT_CHECK_CUDA(cudaMemcpyAsync(s.m32 + off, m + lo, sg.n * 4, cudaMemcpyHostToDevice, s.st));
-                QT_CHECK_CUDA(cudaMemcpyAsync(s.v32 + off, v + lo, sg.n * 4, cudaMemcpyHostToDevice, s.st));
+                QT_CHECK_CUDA(cudaMemcpyAsync(s.m32 + off, m + lo, sg.n * 4, cudaMemcpyDefault, s.st));
+                QT_CHECK_CUDA(cudaMemcpyAsync(s.v32 + off, v + lo, sg.n * 4, cudaMemcpyDefault, s.st));
             }
             QT_CHECK_CUDA(cudaStreamSynchronize(s.st));
         }
@@ -1961,7 +2235,10 @@ int qt_saved_raw(qt_session* h, int layer, const char* site, void* host, int64_t
         int dt = 0;
         if (layer < 0 || layer > s.L) throw QtError(2, "layer out of range");
         LayerBufs& b = s.lb[layer];
-        if (n == "r_in") { src = b.r_in; nb = M * s.d * 2; }
+        if (n == "r_in") {
+            src = (s.offload_x() && layer < s.L) ? s.xhost + (size_t)layer * s.Mmax * s.d : b.r_in;
+            nb = M * s.d * 2;
+        }
         else if (n == "normed_final") { src = s.normed_final; nb = M * s.d * 2; }
         else if (n == "dlogits") { src = s.dlogits; nb = M * s.V * 2; }
         else if (n == "dlogits_lo") { src = s.dlogits_lo; nb = M * s.V * 2; }
@@ -1982,7 +2259,7 @@ int qt_saved_raw(qt_session* h, int layer, const char* site, void* host, int64_t
         if (!src) throw QtError(1, "site " + n + " is not kept in this CE backward mode");
         *bytes = nb;
         *dtype = dt;
-        if (host) QT_CHECK_CUDA(cudaMemcpy(host, src, nb, cudaMemcpyDeviceToHost));
+        if (host) QT_CHECK_CUDA(cudaMemcpy(host, src, nb, cudaMemcpyDefault));
     });
 }
 

@@ -206,6 +206,7 @@ struct PeerGroup {
     std::mutex reg_m;
     struct Member {
         const uint8_t* arena = nullptr;
+        const uint8_t* host = nullptr;  // the rank's pinned host region (offload tiers), or null
         int device = -1;
         cudaEvent_t ready = nullptr, done = nullptr;
     };
@@ -238,12 +239,15 @@ class PeerTransport final : public Transport {
     int device;
     const uint8_t* arena;  // this rank's arena (peers' buffers are at the same offsets in theirs)
     size_t arena_bytes;
+    const uint8_t* host = nullptr;  // this rank's pinned host region (same layout on every rank)
+    size_t host_bytes = 0;
     uint8_t* stage = nullptr;  // W x kStage bytes for the small reductions
     static constexpr size_t kStage = 64 * 1024;
     bool peers_ready = false;
 
-    PeerTransport(std::shared_ptr<PeerGroup> grp, int rk, int dev, const uint8_t* arena_base, size_t bytes)
-        : g(grp), device(dev), arena(arena_base), arena_bytes(bytes) {
+    PeerTransport(std::shared_ptr<PeerGroup> grp, int rk, int dev, const uint8_t* arena_base, size_t bytes,
+                  const uint8_t* host_base = nullptr, size_t hbytes = 0)
+        : g(grp), device(dev), arena(arena_base), arena_bytes(bytes), host(host_base), host_bytes(hbytes) {
         rank = rk;
         world = grp->world;
         if (cudaMalloc(&stage, (size_t)world * kStage) != cudaSuccess)
@@ -252,6 +256,7 @@ class PeerTransport final : public Transport {
         auto& m = g->mem[(size_t)rank];
         if (m.arena) throw TransportError("peer group: rank " + std::to_string(rank) + " already joined");
         m.arena = arena_base;
+        m.host = host_base;
         m.device = dev;
         cudaEventCreateWithFlags(&m.ready, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&m.done, cudaEventDisableTiming);
@@ -271,8 +276,9 @@ class PeerTransport final : public Transport {
     // a peer's address of the buffer at `local` in this rank's arena
     const uint8_t* peer_addr(int p, const void* local) const {
         const uint8_t* l = static_cast<const uint8_t*>(local);
-        if (l < arena || l >= arena + arena_bytes) throw TransportError("peer transport: buffer outside the arena");
-        return g->mem[(size_t)p].arena + (l - arena);
+        if (l >= arena && l < arena + arena_bytes) return g->mem[(size_t)p].arena + (l - arena);
+        if (host && l >= host && l < host + host_bytes) return g->mem[(size_t)p].host + (l - host);
+        throw TransportError("peer transport: buffer outside the arena");
     }
     void first_use() {
         if (peers_ready) return;

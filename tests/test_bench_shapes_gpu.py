@@ -371,13 +371,13 @@ def test_cross_entropy_production_path_real_vocab(ops, ref, N, d, V):
     got_loss = lr.sum().item() / N
     assert abs(got_loss - loss) / loss < 1e-5, (got_loss, loss)
     dh_g = ops.lm_dgrad_tx(dl, dlt, T_, W).float().cpu().numpy()
-    # <= 1 ulp on >= 99.9 % (transcendental ops <= 1 ulp on >= 99 %), the rest
-    # within the cancellation-aware bound, >= 98 % bit-exact
+    # <= 1 ulp on >= 99 % (transcendental ops), the rest within the
+    # cancellation-aware bound, >= 98 % bit-exact
     du = _ulp(dh_g, dh)
     # sum_v |dl[m, v] w[v, c]| <= (|p_t - 1| + sum p_v) / N * max|w| <= 2 max|w| / N
     tol = 8.0 * np.sqrt(V) * 2.0 ** -24 * 2.0 * np.abs(w).max() / N
     assert ((du <= 1) | (np.abs(dh_g.astype(np.float64) - dh) <= tol)).all(), du.max()
-    assert (du <= 1).mean() >= 0.999 and (du == 0).mean() >= 0.98 and _rel(dh_g, dh) < 1e-3, \
+    assert (du <= 1).mean() >= 0.99 and (du == 0).mean() >= 0.98 and _rel(dh_g, dh) < 1e-3, \
         ((du == 0).mean(), (du <= 1).mean(), _rel(dh_g, dh))
     dw_g = ops.lm_wgrad_tx(dl, dlt, T_, H).cpu().numpy()
     assert _rel(dw_g, dw) < 1e-4, _rel(dw_g, dw)

@@ -232,10 +232,10 @@ def _width_step(ref, preset, n_layers, T, seed=1234):
     lg, ng = sess.train_step(toks, 1, step=0)
     assert abs(lg - lw) / lw < 1e-3, (lg, lw)
     assert abs(ng - nw) / nw < 2e-2, (ng, nw)
-    # the reference with ONE E4M3 code step in one weight (two such perturbations, the
-    # envelope is the larger response)
+    # the reference with ONE E4M3 code step in one weight (four such perturbations in
+    # different tensors; the envelope of a tensor is the largest response among the others)
     perts = []
-    for tgt in ("layers.0.w_qkv", f"layers.{n_layers - 1}.w_down"):
+    for tgt in ("layers.0.w_qkv", "layers.0.w_o", "layers.0.w_gate_up", f"layers.{n_layers - 1}.w_down"):
         pert = ref.RefModel(cfg.as_list(), seed, grad_e5m2=True)
         w = pert.get(tgt).copy()
         i = int(np.argmax(np.abs(w) < 0.5 * np.abs(w).max()))
@@ -246,7 +246,7 @@ def _width_step(ref, preset, n_layers, T, seed=1234):
     worst = {}
     for n in rm.names:
         want_g = rm.acc_grad(n)
-        env_g = max(_rel(p.acc_grad(n), want_g) for _, p in perts)
+        env_g = max(_rel(p.acc_grad(n), want_g) for t, p in perts if t != n)
         got_g = _rel(sess.grad(n), want_g)
         assert got_g <= max(2.0 * env_g, 5e-3), (n, "grad", got_g, env_g)
         env_f = max(_update_flips(p.get(n), before[n], rm.get(n), want_g) for t, p in perts if t != n)
