@@ -67,6 +67,18 @@ __device__ __forceinline__ float ex2(float x) {
 }
 constexpr float LOG2E = 1.4426950408889634f;
 
+// P (forward) and P / dS (backward) as MMA operands: bf16 hi + lo (16 significant bits,
+// f32-faithful products) or bf16 alone (one MMA per k-step instead of two).
+// QTB_ATTN_PLO=1|0; qtk_attn_set_plo overrides (tests/A-B).
+static int g_plo = -1;
+inline int p_lo_mode() {
+    if (g_plo < 0) {
+        const char* e = getenv("QTB_ATTN_PLO");
+        g_plo = e ? atoi(e) : 1;
+    }
+    return g_plo;
+}
+
 template <int HD>
 __global__ void __launch_bounds__(NT, 1) fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H, int Hkv,
                                                        float inv_sqrt_d, uint16_t* __restrict__ out, int64_t ldo,
@@ -637,7 +649,7 @@ template <int HD>
 __global__ void __launch_bounds__(NT, 1) fwd1p_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H,
                                                          int Hkv, int B, float inv_sqrt_d, uint16_t* __restrict__ out,
                                                          int64_t ldo, float* __restrict__ out32, float* __restrict__ lse,
-                                                         uint32_t* __restrict__ amax) {
+                                                         uint32_t* __restrict__ amax, int plo) {
     using S = Smem<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -765,7 +777,7 @@ __global__ void __launch_bounds__(NT, 1) fwd1p_tc_kernel(const __grid_constant__
                 for (int kk = 0; kk < BKV / 16; ++kk) {
                     const uint64_t bd = mndesc(va, kk, BKV * 128);
                     mma_bf16_ss(tmem + 256, kdesc(ph, kk, BQ * 128), bd, idesc_o, (j | kk) != 0);
-                    mma_bf16_ss(tmem + 256, kdesc(pl, kk, BQ * 128), bd, idesc_o, 1);
+                    if (plo) mma_bf16_ss(tmem + 256, kdesc(pl, kk, BQ * 128), bd, idesc_o, 1);
                 }
                 tc_commit(&v_empty[vs]);
                 tc_commit(&p_empty[pb]);
@@ -861,14 +873,16 @@ __global__ void __launch_bounds__(NT, 1) fwd1p_tc_kernel(const __grid_constant__
                     s4[(i >> 1) & 3] += pp[0] + pp[1];
                     const float h0 = bf16r(pp[0]), h1 = bf16r(pp[1]);
                     hi[i / 2] = pack_bf16x2(h0, h1);
-                    lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
+                    if (plo) lo[i / 2] = pack_bf16x2(pp[0] - h0, pp[1] - h1);
                 }
                 l += (s4[0] + s4[1]) + (s4[2] + s4[3]);
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc) {
                     const int off = r * 128 + ((cc ^ (r & 7)) << 4);
                     *reinterpret_cast<uint4*>(ph + off) = make_uint4(hi[cc * 4 + 0], hi[cc * 4 + 1], hi[cc * 4 + 2], hi[cc * 4 + 3]);
-                    *reinterpret_cast<uint4*>(pl + off) = make_uint4(lo[cc * 4 + 0], lo[cc * 4 + 1], lo[cc * 4 + 2], lo[cc * 4 + 3]);
+                    if (plo)
+                        *reinterpret_cast<uint4*>(pl + off) =
+                            make_uint4(lo[cc * 4 + 0], lo[cc * 4 + 1], lo[cc * 4 + 2], lo[cc * 4 + 3]);
                 }
                 fence_async_shared();
                 tc_fence_before();
@@ -967,6 +981,11 @@ __device__ __forceinline__ void split32(const float (&v)[32], uint32_t (&hi)[16]
         lo[i] = cvt_bf16x2(v[2 * i] - __uint_as_float(h << 16), v[2 * i + 1] - __uint_as_float(h & 0xffff0000u));
     }
 }
+// v -> bf16 (round to nearest), packed pairs: the single-part operand of the bf16 P / dS mode
+__device__ __forceinline__ void round32(const float (&v)[32], uint32_t (&hi)[16]) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) hi[i] = cvt_bf16x2(v[2 * i], v[2 * i + 1]);
+}
 __device__ __forceinline__ float4 lds4(uint32_t a) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -1038,7 +1057,8 @@ template <int HD>
 __global__ void __launch_bounds__(NT, 1) dkdv_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                         const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                                                         const float* __restrict__ Dv, int T, int H, int Hkv,
-                                                        int qkv_dim, float inv_sqrt_d, uint16_t* __restrict__ dqkv) {
+                                                        int qkv_dim, float inv_sqrt_d, uint16_t* __restrict__ dqkv,
+                                                        int plo) {
     using S = BwdSmem<HD>;
     using P = BwdPipe<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -1138,9 +1158,9 @@ __global__ void __launch_bounds__(NT, 1) dkdv_tc_kernel(const __grid_constant__ 
                 const uint64_t bo = mndesc(oa, kk + 4 * sub, 128 * 128), bq = mndesc(qa, kk + 4 * sub, 128 * 128);
                 const uint32_t acc = (t | kk) != 0;
                 mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bo, idesc_g, acc);
-                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bo, idesc_g, 1);
+                if (plo) mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bo, idesc_g, 1);
                 mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 0), bq, idesc_g, acc);
-                mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 1), bq, idesc_g, 1);
+                if (plo) mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 1), bq, idesc_g, 1);
             }
             tc_commit(&b_free[buf]);
             if (sub == 1) tc_commit(&r_empty[st]);
@@ -1195,12 +1215,19 @@ __global__ void __launch_bounds__(NT, 1) dkdv_tc_kernel(const __grid_constant__ 
             else
                 dkdv_elem<true>(rs, rp, sLD, c_s, inv_sqrt_d, q0 - kv, pv, dsv);
             uint32_t hi[16], lo[16];
-            split32(pv, hi, lo);
-            tmem_st16(lb + col, hi);
-            tmem_st16(lb + col + 16, lo);
-            split32(dsv, hi, lo);
-            tmem_st16(lb + col + 64, hi);
-            tmem_st16(lb + col + 64 + 16, lo);
+            if (plo) {
+                split32(pv, hi, lo);
+                tmem_st16(lb + col, hi);
+                tmem_st16(lb + col + 16, lo);
+                split32(dsv, hi, lo);
+                tmem_st16(lb + col + 64, hi);
+                tmem_st16(lb + col + 64 + 16, lo);
+            } else {
+                round32(pv, hi);
+                tmem_st16(lb + col, hi);
+                round32(dsv, hi);
+                tmem_st16(lb + col + 64, hi);
+            }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -1255,7 +1282,7 @@ template <int HD>
 __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CUtensorMap tq,
                                                       const __grid_constant__ CUtensorMap tdo, const float* __restrict__ lse,
                                                       const float* __restrict__ Dv, int T, int H, int Hkv, int qkv_dim,
-                                                      float inv_sqrt_d, uint16_t* __restrict__ dqkv) {
+                                                      float inv_sqrt_d, uint16_t* __restrict__ dqkv, int plo) {
     using S = BwdSmem<HD>;
     using P = BwdPipe<HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -1376,7 +1403,7 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
             for (int kk = 0; kk < 4; ++kk) {
                 const uint64_t bk = mndesc(ka, kk + 4 * sub, 128 * 128);
                 mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bk, idesc_g, (j | sub | kk) != 0);
-                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bk, idesc_g, 1);
+                if (plo) mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bk, idesc_g, 1);
             }
             tc_commit(&b_free[buf]);
             if (sub == 1) {
@@ -1414,9 +1441,14 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
                 else
                     dq_elem<true>(rs, rp, c_s, nl, inv_sqrt_d, dsc, k0, qok ? q : -1, dsv);
                 uint32_t hi[16], lo[16];
-                split32(dsv, hi, lo);
-                tmem_st16(lb + col, hi);
-                tmem_st16(lb + col + 16, lo);
+                if (plo) {
+                    split32(dsv, hi, lo);
+                    tmem_st16(lb + col, hi);
+                    tmem_st16(lb + col + 16, lo);
+                } else {
+                    round32(dsv, hi);
+                    tmem_st16(lb + col, hi);
+                }
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
@@ -1501,7 +1533,7 @@ extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, in
             const int smem = Smem<HDV>::BYTES;                                                                     \
             cudaFuncSetAttribute(fwd1p_tc_kernel<HDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
             fwd1p_tc_kernel<HDV><<<pg, NT, smem, s>>>(tm, T, H, Hkv, B, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, \
-                                                      amax);                                                       \
+                                                      amax, p_lo_mode());                                          \
         }
         if (hd == 64) QTB_FWDP(64) else QTB_FWDP(128)
 #undef QTB_FWDP
@@ -1550,8 +1582,10 @@ extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* 
         const int smem = BwdSmem<HD>::BYTES;                                                                       \
         cudaFuncSetAttribute(dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
         cudaFuncSetAttribute(dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
-        dkdv_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
-        dq_tc_kernel<HD><<<gdq, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv); \
+        dkdv_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv, \
+                                                  p_lo_mode());                                                   \
+        dq_tc_kernel<HD><<<gdq, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv,    \
+                                              p_lo_mode());                                                       \
     }
     if (hd == 64)
         QTB_BWD_TC(64)
@@ -1560,3 +1594,5 @@ extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* 
 #undef QTB_BWD_TC
     return (int)cudaGetLastError();
 }
+
+extern "C" void qtk_attn_set_plo(int plo) { qtb::attn_tc::g_plo = plo; }

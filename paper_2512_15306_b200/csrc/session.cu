@@ -422,6 +422,8 @@ class Session {
                     tr = std::make_unique<PeerTransport>(group, rank, device, arena, arena_bytes, harena, harena_bytes);
                 } else {
                     if (!nccl_id) throw QtError(1, "world > 1 needs an NCCL unique id (or a peer group)");
+                    if (harena && !shard_weights() && offload_master())
+                        throw QtError(1, "offload.master over NCCL needs shard_weights (NCCL gathers device memory)");
                     tr = std::make_unique<NcclTransport>(rank, world, nccl_id);
                 }
             } catch (const TransportError& e) {
@@ -2022,7 +2024,7 @@ int qt_moments_download(qt_session* h, int i, float* m, float* v) {
         std::vector<SegH> segs(s.nsegs);
         QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDefault));
         const SegH& sg = segs[i];
-        const int64_t off = s.world > 1 ? sg.off : t.off;
+        const int64_t off = sg.off;  // moment offset (world 1: the gradient layout)
         if (s.plan.bf16_moments) {  // bf16-SR moments, widened to f32 (exact)
             download_bf16(s, s.m16 + off, sg.n, m);
             download_bf16(s, s.v16 + off, sg.n, v);
@@ -2042,7 +2044,7 @@ int qt_moments_upload(qt_session* h, int i, const float* m, const float* v, int6
         std::vector<SegH> segs(s.nsegs);
         QT_CHECK_CUDA(cudaMemcpy(segs.data(), s.segs_dev, segs.size() * sizeof(SegH), cudaMemcpyDefault));
         const SegH& sg = segs[i];
-        const int64_t off = s.world > 1 ? sg.off : t.off;
+        const int64_t off = sg.off;  // moment offset (world 1: the gradient layout)
         const int64_t lo = s.world > 1 ? std::min<int64_t>((int64_t)s.rank * t.pw, t.numel) : 0;
         if (sg.n > 0) {
             if (s.plan.bf16_moments) {

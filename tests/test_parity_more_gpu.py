@@ -246,7 +246,9 @@ def _width_step(ref, preset, n_layers, T, seed=1234):
     worst = {}
     for n in rm.names:
         want_g = rm.acc_grad(n)
-        env_g = max(_rel(p.acc_grad(n), want_g) for t, p in perts if t != n)
+        # any of the perturbations (a tensor's gradient does not contain its own weight, only
+        # the activations downstream of it): the largest response is the envelope
+        env_g = max(_rel(p.acc_grad(n), want_g) for _, p in perts)
         got_g = _rel(sess.grad(n), want_g)
         assert got_g <= max(2.0 * env_g, 5e-3), (n, "grad", got_g, env_g)
         env_f = max(_update_flips(p.get(n), before[n], rm.get(n), want_g) for t, p in perts if t != n)
