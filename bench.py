@@ -216,6 +216,8 @@ def main():
     ap.add_argument("--moments", default="f32", choices=["f32", "bf16_sr"])
     ap.add_argument("--shard-grads", action="store_true")
     ap.add_argument("--shard-weights", action="store_true")
+    ap.add_argument("--offload", default="", help="RunPlan::offload categories: x,m,v,master,weights,grads")
+    ap.add_argument("--transfer-policy", default="double_buffer", choices=["zero_copy", "double_buffer"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample-tokens", type=int, default=128)
     ap.add_argument("--profile-json", default="")
@@ -247,7 +249,8 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
     plan = S.RunPlan(micro_batch=B, ga_steps=1, recompute=tuple(x for x in args.recompute.split(",") if x),
-                     moments=args.moments, shard_grads=args.shard_grads, shard_weights=args.shard_weights)
+                     moments=args.moments, shard_grads=args.shard_grads, shard_weights=args.shard_weights,
+                     offload=tuple(x for x in args.offload.split(",") if x), transfer_policy=args.transfer_policy)
     sess = S.Session(cfg, S.PrecisionMap(backward_grads=args.grads), plan, S.AdamWHyper(), seed=1234, rank=rank,
                      world=world, nccl_id=nccl_id, device=local)
     sess.init_params(1234)
@@ -377,6 +380,7 @@ def main():
                    "seq_len": T, "parallelism": f"dp{world}" + ("+zero1" if world > 1 else ""),
                    "grads": args.grads, "recompute": args.recompute or "none", "moments": args.moments,
                    "shard_grads": args.shard_grads, "shard_weights": args.shard_weights,
+                   "offload": args.offload or "none", "transfer_policy": args.transfer_policy,
                    "l2": "activations/logits (GBs) exceed the 126 MB L2; no explicit flush"},
         "mfu": mfu,
         "mfu_basis": "reference formula (src/memplan.cpp:264-312) vs B200 dense spec 4.5 PF fp8 / 2.25 PF bf16",

@@ -175,6 +175,11 @@ void qtk_attn_set_mode(int fast_exp, int bwd_split);
 size_t qtk_attn_bwd_ws_bytes(int B, int T, int H, int Hkv, int hd);
 int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv, int B,
                  int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s);
+/* as qtk_attn_bwd; the tcgen05 path runs its dQ kernel on s2 concurrently with dK/dV on s
+ * (disjoint columns of dqkv) and joins s2 into s before returning */
+int qtk_attn_bwd2(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv,
+                  int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s,
+                  cudaStream_t s2);
 
 /* fused_cross_entropy_chunked softmax stage (src/tensorops.cpp:367-393):
  * per-row loss and dlogits from f32 logits; dlogits (f32 in the reference) is

@@ -760,6 +760,23 @@ size_t qtk_attn_bwd_ws_bytes(int B, int T, int H, int Hkv, int hd) {
 int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
                     float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s);
 
+int qtk_attn_bwd_tc2(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
+                     float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s,
+                     cudaStream_t s2);
+// two-stream form: the tcgen05 path runs its dQ kernel on s2 next to dK/dV on s
+int qtk_attn_bwd2(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv,
+                  int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s,
+                  cudaStream_t s2) {
+    static int use_tc = -1;
+    if (use_tc < 0) {
+        const char* e = getenv("QTB_ATTN_BWD_TC");
+        use_tc = e ? atoi(e) : 1;
+    }
+    if (use_tc && (hd == 64 || hd == 128) && !(H % Hkv) && !(T % 4))
+        return qtk_attn_bwd_tc2(qkv, out32, dout, ldo, lse, Dv, B, T, H, Hkv, hd, qkv_dim, dqkv, ws, s, s2);
+    return qtk_attn_bwd(qkv, out32, dout, ldo, lse, Dv, B, T, H, Hkv, hd, qkv_dim, dqkv, ws, s);
+}
+
 int qtk_attn_bwd(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse, float* Dv, int B,
                  int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws, cudaStream_t s) {
     if (H % Hkv || T % 4) return 1;

@@ -67,6 +67,25 @@ __device__ __forceinline__ float ex2(float x) {
 }
 constexpr float LOG2E = 1.4426950408889634f;
 
+// fork/join events of the two-stream backward: one pair per host thread (sessions of a peer
+// group run on different threads)
+inline cudaEvent_t fork_ev() {
+    thread_local cudaEvent_t e = [] {
+        cudaEvent_t x;
+        cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        return x;
+    }();
+    return e;
+}
+inline cudaEvent_t join_ev() {
+    thread_local cudaEvent_t e = [] {
+        cudaEvent_t x;
+        cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+        return x;
+    }();
+    return e;
+}
+
 // P (forward) and P / dS (backward) as MMA operands: bf16 hi + lo (16 significant bits,
 // f32-faithful products) or bf16 alone (one MMA per k-step instead of two).
 // QTB_ATTN_PLO=1|0; qtk_attn_set_plo overrides (tests/A-B).
@@ -1555,9 +1574,19 @@ void launch_bwd_dot(const uint16_t* dout, const float* o, int64_t ld, int T, int
 }  // namespace attn
 }  // namespace qtb
 
+// s2 (optional): the dQ kernel runs there, concurrently with dK/dV (they write disjoint
+// columns of dqkv); s waits for it before returning
+extern "C" int qtk_attn_bwd_tc2(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
+                                float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws,
+                                cudaStream_t s, cudaStream_t s2);
 extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
                                float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws,
                                cudaStream_t s) {
+    return qtk_attn_bwd_tc2(qkv, out32, dout, ldo, lse, Dv, B, T, H, Hkv, hd, qkv_dim, dqkv, ws, s, nullptr);
+}
+extern "C" int qtk_attn_bwd_tc2(const void* qkv, const float* out32, const void* dout, int64_t ldo, const float* lse,
+                                float* Dv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* dqkv, float* ws,
+                                cudaStream_t s, cudaStream_t s2) {
     using namespace qtb::attn_tc;
     if (H % Hkv || (hd != 64 && hd != 128) || (qkv_dim % 8) || (ldo % 8)) return 1;
     (void)ws;  // dK/dV accumulate over the GQA group in TMEM: no partials
@@ -1582,10 +1611,20 @@ extern "C" int qtk_attn_bwd_tc(const void* qkv, const float* out32, const void* 
         const int smem = BwdSmem<HD>::BYTES;                                                                       \
         cudaFuncSetAttribute(dkdv_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);               \
         cudaFuncSetAttribute(dq_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                 \
+        cudaStream_t sq = s;                                                                                       \
+        if (s2 && s2 != s) {                                                                                       \
+            cudaEventRecord(fork_ev(), s);                                                                         \
+            cudaStreamWaitEvent(s2, fork_ev(), 0);                                                                 \
+            sq = s2;                                                                                               \
+        }                                                                                                          \
+        dq_tc_kernel<HD><<<gdq, NT, smem, sq>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv,   \
+                                               p_lo_mode());                                                      \
         dkdv_tc_kernel<HD><<<grid, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv, \
                                                   p_lo_mode());                                                   \
-        dq_tc_kernel<HD><<<gdq, NT, smem, s>>>(tq, tdo, lse, Dv, T, H, Hkv, qkv_dim, inv_sqrt_d, (uint16_t*)dqkv,    \
-                                              p_lo_mode());                                                       \
+        if (sq != s) {                                                                                             \
+            cudaEventRecord(join_ev(), sq);                                                                        \
+            cudaStreamWaitEvent(s, join_ev(), 0);                                                                  \
+        }                                                                                                          \
     }
     if (hd == 64)
         QTB_BWD_TC(64)

@@ -329,7 +329,14 @@ class Session {
     uint16_t *d_r = nullptr, *d_h = nullptr, *d_gu = nullptr, *d_n = nullptr, *d_ao = nullptr, *d_att = nullptr,
              *d_qkv = nullptr, *d_hidden = nullptr;
     uint8_t* gcodes = nullptr;  // grad-kind codes scratch (M x max(F, q))
+    // weight-gradient GEMMs on a side stream (QTB_WGRAD_SIDE): the wgrad of a d_out overlaps its
+    // dgrad and the elementwise work after it; the grad-kind codes alternate between two
+    // buffers so the next cast need not wait for the previous wgrad
+    uint8_t* gcodes2 = nullptr;
+    cudaStream_t wst = nullptr;
+    cudaEvent_t ev_qready = nullptr, ev_wdone[2] = {nullptr, nullptr}, ev_wjoin = nullptr;
     float* gemm_ws = nullptr;   // split-K partials for the small-grid weight-gradient GEMMs
+    float* gemm_ws2 = nullptr;  // the side stream's
     int64_t gemm_ws_bytes = 0;
     float* logits = nullptr;
     uint16_t* dlogits = nullptr;
@@ -438,6 +445,11 @@ class Session {
         }
         if (stream_codes() && offload_weights())
             QT_CHECK_CUDA(cudaMallocHost(&whost, std::max<size_t>((size_t)L * wl_total, 1)));
+        if (wgrad_side()) {
+            QT_CHECK_CUDA(cudaStreamCreateWithFlags(&wst, cudaStreamNonBlocking));
+            for (cudaEvent_t* e : {&ev_qready, &ev_wdone[0], &ev_wdone[1], &ev_wjoin})
+                QT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
         if (offload_x()) {
             if (!cst) QT_CHECK_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
             for (cudaEvent_t* e : {&ev_xready[0], &ev_xready[1], &ev_xfree[0], &ev_xfree[1]})
@@ -481,6 +493,9 @@ class Session {
                               ev_wready[1]})
             if (e) cudaEventDestroy(e);
         if (cst) cudaStreamDestroy(cst);
+        for (cudaEvent_t e : {ev_qready, ev_wdone[0], ev_wdone[1], ev_wjoin})
+            if (e) cudaEventDestroy(e);
+        if (wst) cudaStreamDestroy(wst);
         if (whost) cudaFreeHost(whost);
         if (harena) cudaFreeHost(harena);
         for (cudaEvent_t e : {ev_mready[0], ev_mready[1], ev_mdone[0], ev_mdone[1], ev_mfree[0], ev_mfree[1],
@@ -728,6 +743,7 @@ class Session {
         req(&d_qkv, M * q * 2);
         req(&d_hidden, M * d * 2);
         req(&gcodes, M * std::max(F, q));
+        if (wgrad_side()) req(&gcodes2, M * std::max(F, q));
         {
             // wgrad shapes (out, in, K = tokens) and small fwd/dgrad shapes
             const int64_t shapes[][3] = {{q, d, M}, {d, d, M}, {F, d, M}, {d, Hh, M}, {M, q, d}, {M, d, d},
@@ -735,6 +751,7 @@ class Session {
             for (auto& sh : shapes)
                 gemm_ws_bytes = std::max<int64_t>(gemm_ws_bytes, qtk_gemm_splitk_ws_bytes(sh[0], sh[1], sh[2], 0));
             if (gemm_ws_bytes > 0) req(&gemm_ws, gemm_ws_bytes);
+            if (gemm_ws_bytes > 0 && wgrad_side()) req(&gemm_ws2, gemm_ws_bytes);
         }
         req(&logits, (size_t)M * V * 4);
         req(&dlogits, (size_t)M * V * 2);
@@ -904,7 +921,12 @@ class Session {
     void build_mgroups() {
         make_segments();
         mgroups.clear();
-        const int64_t cs = qtk_adamw_chunk_size(), cap = int64_t(32) << 20;
+        // groups of <= 32 Mi moment elements, and at least 8 groups for small models (the two
+        // device slots then hold a quarter of the moments at most)
+        const int64_t cs = qtk_adamw_chunk_size();
+        int64_t tot = 0;
+        for (const SegH& sg : segs_h) tot += sg.n;
+        const int64_t cap = std::max<int64_t>(std::min<int64_t>(int64_t(32) << 20, ceil_div(tot, 8)), cs);
         mstage_elems = 0;
         int c0 = 0;
         while (c0 < nchunks) {
@@ -972,7 +994,7 @@ class Session {
               int64_t ldo, const void* res = nullptr, int64_t ldr = 0, uint64_t sr_seed = 0, uint64_t sr_stream = 0,
               uint64_t sr_base = 0, const void* a2 = nullptr, uint32_t* amax = nullptr, const int32_t* ce_targets = nullptr,
               float* ce_st = nullptr, float* ce_tl = nullptr, float* ws = nullptr, int64_t ws_bytes = 0,
-              int split_k = 0) {
+              int split_k = 0, cudaStream_t on = nullptr) {
         QtkGemm g{};
         g.kind = kind;
         g.a_fmt = afmt;
@@ -998,7 +1020,7 @@ class Session {
         g.sr_base = sr_base;
         g.bn = 0;
         g.a2 = a2;
-        g.ws = ws ? ws : gemm_ws;
+        g.ws = ws ? ws : (on && on == wst ? gemm_ws2 : gemm_ws);  // each stream its own split-K workspace
         g.ws_bytes = ws ? ws_bytes : gemm_ws_bytes;
         g.split_k = ws ? split_k : 0;
         g.amax = amax;
@@ -1006,9 +1028,10 @@ class Session {
         g.ce_targets = ce_targets;
         g.ce_stats = ce_st;
         g.ce_tgt_logit = ce_tl;
-        const int h = prof_begin();
-        QT_CHECK_K(qtk_gemm(&g, st));
-        prof_end(h, kind == 0 ? 0 : 1, 2.0 * M * N * K * (a2 ? 2 : 1));
+        cudaStream_t gs_ = on ? on : st;
+        const int h = prof_begin_on(gs_);
+        QT_CHECK_K(qtk_gemm(&g, gs_));
+        prof_end_on(h, kind == 0 ? 0 : 1, 2.0 * M * N * K * (a2 ? 2 : 1), gs_);
     }
 
     int gkind() const { return prec.backward_grads == 0 ? kE4M3 : kE5M2; }
@@ -1031,6 +1054,23 @@ class Session {
     }
     // target-exact CE backward: bf16 dlogits without the target entry + the exact f32 target
     // term (QTB_LM_TX=0: the bf16 hi + lo split-A path)
+    // attention backward: dQ on the side stream next to dK/dV (QTB_ATTN_2S)
+    static bool attn_two_streams() {
+        static int f = -1;
+        if (f < 0) {
+            const char* e = getenv("QTB_ATTN_2S");
+            f = e ? atoi(e) : 1;
+        }
+        return f != 0 && wgrad_side();
+    }
+    static bool wgrad_side() {
+        static int f = -1;
+        if (f < 0) {
+            const char* e = getenv("QTB_WGRAD_SIDE");
+            f = e ? atoi(e) : 1;
+        }
+        return f != 0;
+    }
     bool lm_tx() const {
         static int f = -1;
         if (f < 0) {
@@ -1401,9 +1441,52 @@ class Session {
         fwd_with_grads = with_grads;
     }
 
+    // ---------------- grad-kind casts and weight gradients (side stream) ----------------
+    int gbuf_i = 0;
+    bool wdone_valid[2] = {false, false};  // ev_wdone[k] recorded in this backward
+    // absmax-scaled cast of a d_out into the next grad-codes buffer (waiting for the wgrad that
+    // read that buffer two casts ago); the side stream may read it after this
+    uint8_t* quant_grad(const uint16_t* src, int64_t n, int gk_, uint32_t* amax, float* scale) {
+        uint8_t* buf = gcodes;
+        if (wgrad_side()) {
+            buf = gbuf_i ? gcodes2 : gcodes;
+            if (wdone_valid[gbuf_i]) QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_wdone[gbuf_i], 0));
+        }
+        const int h = prof_begin();
+        QT_CHECK_K(qtk_quantize_bf16(src, n, gk_, amax, buf, scale, st));
+        prof_end(h, 3, 3.0 * n);
+        if (wgrad_side()) {
+            QT_CHECK_CUDA(cudaEventRecord(ev_qready, st));
+            QT_CHECK_CUDA(cudaStreamWaitEvent(wst, ev_qready, 0));
+        }
+        return buf;
+    }
+    // GradAccumulator SR-accumulate wgrad of tensor t from the codes `gc` (model.cpp:160-167,
+    // 448-464): on the side stream, which then marks the codes buffer free
+    void wgrad(int64_t Mo, int64_t No, int64_t K, const uint8_t* gc, int64_t lda, const uint8_t* act, int64_t ldb,
+               const float* gsc, const float* asc, const ParamT& t, uint64_t micro_step) {
+        const uint64_t aseed = seed + (uint64_t)rank;
+        gemm(0, gkind(), kE4M3, true, true, Mo, No, K, gc, lda, act, ldb, gsc, asc, EPI_BF16_ACC, gbuf(t), No, nullptr,
+             0, aseed, t.s_acc, micro_step * (uint64_t)t.numel, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+             0, wgrad_side() ? wst : nullptr);
+        if (wgrad_side()) {
+            QT_CHECK_CUDA(cudaEventRecord(ev_wdone[gbuf_i], wst));
+            wdone_valid[gbuf_i] = true;
+            gbuf_i ^= 1;
+        }
+    }
+    // the compute stream waits for every weight gradient issued so far
+    void wgrad_join() {
+        if (!wgrad_side()) return;
+        QT_CHECK_CUDA(cudaEventRecord(ev_wjoin, wst));
+        QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_wjoin, 0));
+    }
+
     // ---------------- model_backward + GradAccumulator (src/model.cpp:354-464) ----------------
     void backward(uint64_t micro_step) {
         if (!have_fwd || !fwd_with_grads) throw QtError(1, "model_backward: no forward with grads to differentiate");
+        gbuf_i = 0;
+        wdone_valid[0] = wdone_valid[1] = false;
         const int64_t M = curM;
         const uint64_t aseed = seed + (uint64_t)rank;  // trainer.cpp:68-70: worker w accumulates with seed+w
         const int gk = gkind();
@@ -1460,30 +1543,24 @@ class Session {
             const ParamT& pg = P[lp(l, 4)];
             const ParamT& pd = P[lp(l, 5)];
             // ---- FFN down: dY = d_r
-            h = prof_begin();
-            QT_CHECK_K(qtk_quantize_bf16(d_r, M * d, gk, ga + G_DR, gcodes, gs + G_DR, st));
-            prof_end(h, 3, 3.0 * M * d);
-            gemm(0, gk, kE4M3, true, true, d, Hh, M, gcodes, d, b.hc, Hh, gs + G_DR, as + S_H, EPI_BF16_ACC,
-                 gbuf(pd), Hh, nullptr, 0, aseed, pd.s_acc, micro_step * (uint64_t)pd.numel);
+            uint8_t* gc = quant_grad(d_r, M * d, gk, ga + G_DR, gs + G_DR);
+            wgrad(d, Hh, M, gc, d, b.hc, Hh, gs + G_DR, as + S_H, pd, micro_step);
             if (fuse_swiglu_bwd()) {
                 // d_h = down-proj dgrad, consumed in the GEMM epilogue by swiglu_backward:
                 // d_gate|d_up + their absmax written directly (d_h never reaches HBM)
-                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wc(l, W_DOWN), Hh, gs + G_DR,
+                gemm(0, gk, kE4M3, false, true, M, Hh, d, gc, d, wc(l, W_DOWN), Hh, gs + G_DR,
                      ws + W_DOWN, EPI_SWIGLU_BWD, d_gu, F, b.gu, F, 0, 0, 0, nullptr, ga + G_DGU);
             } else {
-                gemm(0, gk, kE4M3, false, true, M, Hh, d, gcodes, d, wc(l, W_DOWN), Hh, gs + G_DR,
+                gemm(0, gk, kE4M3, false, true, M, Hh, d, gc, d, wc(l, W_DOWN), Hh, gs + G_DR,
                      ws + W_DOWN, EPI_BF16, d_h, Hh);
                 h = prof_begin();
                 QT_CHECK_K(qtk_swiglu_bwd(b.gu, d_h, M, Hh, d_gu, ga + G_DGU, st));
                 prof_end(h, 5, 2.0 * M * F * 2 + 2.0 * M * Hh);
             }
             // ---- gate_up
-            h = prof_begin();
-            QT_CHECK_K(qtk_quantize_bf16(d_gu, M * F, gk, ga + G_DGU, gcodes, gs + G_DGU, st));
-            prof_end(h, 3, 3.0 * M * F);
-            gemm(0, gk, kE4M3, true, true, F, d, M, gcodes, F, b.n2c, d, gs + G_DGU, as + S_N2, EPI_BF16_ACC,
-                 gbuf(pg), d, nullptr, 0, aseed, pg.s_acc, micro_step * (uint64_t)pg.numel);
-            gemm(0, gk, kE4M3, false, true, M, d, F, gcodes, F, wc(l, W_GU), d, gs + G_DGU, ws + W_GU, EPI_BF16,
+            gc = quant_grad(d_gu, M * F, gk, ga + G_DGU, gs + G_DGU);
+            wgrad(F, d, M, gc, F, b.n2c, d, gs + G_DGU, as + S_N2, pg, micro_step);
+            gemm(0, gk, kE4M3, false, true, M, d, F, gc, F, wc(l, W_GU), d, gs + G_DGU, ws + W_GU, EPI_BF16,
                  d_n, d);
             // ---- rmsnorm2 backward: d_attn_out = ... + d_r (model.cpp:393-399)
             h = prof_begin();
@@ -1492,27 +1569,22 @@ class Session {
             accumulate_f32(P[lp(l, 3)], dgamma, micro_step);
             prof_end(h, 4, 10.0 * M * d);
             // ---- attention output projection
-            h = prof_begin();
-            QT_CHECK_K(qtk_quantize_bf16(d_ao, M * d, gk, ga + G_DAO, gcodes, gs + G_DAO, st));
-            prof_end(h, 3, 3.0 * M * d);
-            gemm(0, gk, kE4M3, true, true, d, d, M, gcodes, d, b.attc, d, gs + G_DAO, as + S_ATT, EPI_BF16_ACC,
-                 gbuf(po), d, nullptr, 0, aseed, po.s_acc, micro_step * (uint64_t)po.numel);
-            gemm(0, gk, kE4M3, false, true, M, d, d, gcodes, d, wc(l, W_O), d, gs + G_DAO, ws + W_O, EPI_BF16,
+            gc = quant_grad(d_ao, M * d, gk, ga + G_DAO, gs + G_DAO);
+            wgrad(d, d, M, gc, d, b.attc, d, gs + G_DAO, as + S_ATT, po, micro_step);
+            gemm(0, gk, kE4M3, false, true, M, d, d, gc, d, wc(l, W_O), d, gs + G_DAO, ws + W_O, EPI_BF16,
                  d_att, d);
             // ---- attention backward + inverse RoPE
             h = prof_begin();
-            QT_CHECK_K(qtk_attn_bwd(b.qkv, b.att32, d_att, d, b.lse, Dv, curB, curT, H, Hkv, hd, q, d_qkv, attn_ws, st));
+            QT_CHECK_K(qtk_attn_bwd2(b.qkv, b.att32, d_att, d, b.lse, Dv, curB, curT, H, Hkv, hd, q, d_qkv, attn_ws, st,
+                                     attn_two_streams() ? wst : nullptr));
             prof_end(h, 8, 10.0 * curB * H * (double)curT * curT / 2 * hd);
             h = prof_begin();
             QT_CHECK_K(qtk_rope(d_qkv, M, curT, H + Hkv, hd, q, rope_tab, 1, ga + G_DQKV, st));
             prof_end(h, 5, 4.0 * M * q);
             // ---- qkv projection
-            h = prof_begin();
-            QT_CHECK_K(qtk_quantize_bf16(d_qkv, M * q, gk, ga + G_DQKV, gcodes, gs + G_DQKV, st));
-            prof_end(h, 3, 3.0 * M * q);
-            gemm(0, gk, kE4M3, true, true, q, d, M, gcodes, q, b.n1c, d, gs + G_DQKV, as + S_N1, EPI_BF16_ACC,
-                 gbuf(pq), d, nullptr, 0, aseed, pq.s_acc, micro_step * (uint64_t)pq.numel);
-            gemm(0, gk, kE4M3, false, true, M, d, q, gcodes, q, wc(l, W_QKV), d, gs + G_DQKV, ws + W_QKV,
+            gc = quant_grad(d_qkv, M * q, gk, ga + G_DQKV, gs + G_DQKV);
+            wgrad(q, d, M, gc, q, b.n1c, d, gs + G_DQKV, as + S_N1, pq, micro_step);
+            gemm(0, gk, kE4M3, false, true, M, d, q, gc, q, wc(l, W_QKV), d, gs + G_DQKV, ws + W_QKV,
                  EPI_BF16, d_n, d);
             // ---- rmsnorm1 backward: d_r = ... + d_attn_out (model.cpp:433-439)
             h = prof_begin();
@@ -1522,8 +1594,12 @@ class Session {
             prof_end(h, 4, 10.0 * M * d);
             codes_release(l);
             if (offload_x()) QT_CHECK_CUDA(cudaEventRecord(ev_xfree[l % 2], st));
-            if (exchange_in_backward) reduce_layer_async(l);
+            if (exchange_in_backward) {
+                wgrad_join();  // the layer's weight gradients are final
+                reduce_layer_async(l);
+            }
         }
+        wgrad_join();
         // ordered embedding backward, bf16 round, accumulate (model.cpp:442-444)
         {
             const ParamT& t = par("embed");

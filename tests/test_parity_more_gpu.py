@@ -243,19 +243,20 @@ def _width_step(ref, preset, n_layers, T, seed=1234):
         pert.set(tgt, w)
         pert.train_step(toks, 1, step=0)
         perts.append((tgt, pert))
-    worst = {}
+    worst, bad = {}, []
     for n in rm.names:
         want_g = rm.acc_grad(n)
         # any of the perturbations (a tensor's gradient does not contain its own weight, only
         # the activations downstream of it): the largest response is the envelope
         env_g = max(_rel(p.acc_grad(n), want_g) for _, p in perts)
         got_g = _rel(sess.grad(n), want_g)
-        assert got_g <= max(2.0 * env_g, 5e-3), (n, "grad", got_g, env_g)
         env_f = max(_update_flips(p.get(n), before[n], rm.get(n), want_g) for t, p in perts if t != n)
         got_f = _update_flips(sess.download(n), before[n], rm.get(n), want_g)
-        worst[n] = (got_g, env_g, got_f, env_f)
-        assert got_f <= max(2.0 * env_f, 5e-3), (n, "update flips", got_f, env_f)
-    print({n: tuple(round(x, 5) for x in v) for n, v in worst.items()})
+        worst[n] = tuple(round(float(x), 5) for x in (got_g, env_g, got_f, env_f))
+        if got_g > max(2.0 * env_g, 5e-3) or got_f > max(2.0 * env_f, 5e-3):
+            bad.append(n)
+    print(worst)
+    assert not bad, {n: worst[n] for n in bad}
 
 
 def test_train_step_qwen05b_width_2_layers(ref):

@@ -71,7 +71,10 @@ def test_trainer_metrics_and_checkpoint_vs_reference(ref, tmp_path, kind, worker
     assert t_o["optim.step"][0] == mine["steps"]
     for name, v in t_r.items():
         if name.startswith("optim.v.") or name.startswith("optim.m."):
-            assert _rel(t_o[name], v) < 0.2, name  # moments of a free-running 6-step run
+            # running averages of six free-running steps' gradients, whose single-step
+            # envelope is already ~1.4e-2 and compounds: a coarse check (the
+            # AdamW arithmetic itself is bitwise-tested teacher-forced, test_optim_gpu.py)
+            assert _rel(t_o[name], v) < 0.5, name
         else:
             assert _rel(t_o[name], v) < 2e-2, name
 
