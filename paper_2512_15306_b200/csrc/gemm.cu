@@ -818,6 +818,7 @@ TileCfg choose_cfg(int64_t M, int64_t N, int kind, bool b_mn, int64_t K = 1 << 2
     double best_t = 1e30;
     for (int cg = 1; cg <= 2; ++cg) {
         if (forced == 1 && cg == 2) continue;
+        if (forced == 2 && cg == 1 && M >= 256) continue;  // QTB_GEMM_CG=2: pairs whenever legal
         if (cg == 2 && M < 256) continue;
         for (int bn = 128; bn <= 256; bn += 128) {
             if (cg == 2 && kind == 0 && b_mn && bn == 128) continue;  // half-atom MN-major B
