@@ -1444,6 +1444,8 @@ class Session {
     // ---------------- grad-kind casts and weight gradients (side stream) ----------------
     int gbuf_i = 0;
     bool wdone_valid[2] = {false, false};  // ev_wdone[k] recorded in this backward
+    // the full gradient buffer is all zeros (zeroed and not yet accumulated into)
+    bool grads_fresh = false;
     // absmax-scaled cast of a d_out into the next grad-codes buffer (waiting for the wgrad that
     // read that buffer two casts ago); the side stream may read it after this
     uint8_t* quant_grad(const uint16_t* src, int64_t n, int gk_, uint32_t* amax, float* scale) {
@@ -1466,7 +1468,12 @@ class Session {
     void wgrad(int64_t Mo, int64_t No, int64_t K, const uint8_t* gc, int64_t lda, const uint8_t* act, int64_t ldb,
                const float* gsc, const float* asc, const ParamT& t, uint64_t micro_step) {
         const uint64_t aseed = seed + (uint64_t)rank;
-        gemm(0, gkind(), kE4M3, true, true, Mo, No, K, gc, lda, act, ldb, gsc, asc, EPI_BF16_ACC, gbuf(t), No, nullptr,
+        // GradAccumulator into a zero buffer: SR(0 + bf16(acc/(sa*sb))) returns the bf16 value
+        // unchanged (a representable value passes through, numerics.cpp:240-250), so the first
+        // accumulation is the plain rounded store: no read of the buffer, no RNG (same bits)
+        const bool fresh = t.goff < 0 || grads_fresh;
+        gemm(0, gkind(), kE4M3, true, true, Mo, No, K, gc, lda, act, ldb, gsc, asc, fresh ? EPI_BF16 : EPI_BF16_ACC,
+             gbuf(t), No, nullptr,
              0, aseed, t.s_acc, micro_step * (uint64_t)t.numel, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
              0, wgrad_side() ? wst : nullptr);
         if (wgrad_side()) {
@@ -1612,6 +1619,7 @@ class Session {
                                          t.s_acc, micro_step * (uint64_t)t.numel, st));
             prof_end(h, 5, 4.0 * M * d);
         }
+        grads_fresh = false;  // this micro-batch's gradients are in the buffer now
     }
 
     void accumulate_f32(const ParamT& t, const float* g, uint64_t micro_step) {
@@ -1847,6 +1855,7 @@ class Session {
         } in_step_guard(in_step);
         build_step_context();
         QT_CHECK_CUDA(cudaMemsetAsync(grads, 0, g_store * 2, st));
+        grads_fresh = true;
         for (int ga = 0; ga < GA; ++ga) {
             forward(tokens + (int64_t)ga * tokens_per_mb, tokens_per_mb, batch, true);
             QT_CHECK_CUDA(cudaMemcpyAsync(loss_dev + 1 + ga, loss_dev, 4, cudaMemcpyDeviceToDevice, st));
@@ -2212,7 +2221,10 @@ int qt_backward(qt_session* h, uint64_t micro_step) {
 }
 
 int qt_zero_grads(qt_session* h) {
-    return guard([&] { QT_CHECK_CUDA(cudaMemsetAsync(h->s->grads, 0, h->s->g_store * 2, h->s->st)); });
+    return guard([&] {
+        QT_CHECK_CUDA(cudaMemsetAsync(h->s->grads, 0, h->s->g_store * 2, h->s->st));
+        h->s->grads_fresh = true;
+    });
 }
 
 int qt_grad_norm(qt_session* h, double* norm_host) {

@@ -42,7 +42,7 @@ def _rel(a, b):
     return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30)
 
 
-@pytest.mark.parametrize("rows,d", [(1, 64), (37, 256), (300, 896), (64, 4096)])
+@pytest.mark.parametrize("rows,d", [(1, 64), (37, 256), (300, 896), (64, 4096), (200, 4096), (96, 5120)])
 @pytest.mark.parametrize("with_x", [False, True])
 def test_rmsnorm_fwd_bitexact(ops, ref, rows, d, with_x):
     res = rng_floats(rows + d, rows * d, -3, 3).reshape(rows, d)
@@ -56,7 +56,7 @@ def test_rmsnorm_fwd_bitexact(ops, ref, rows, d, with_x):
     assert ops.amax_value(slot) == am_w
 
 
-@pytest.mark.parametrize("rows,d", [(5, 64), (300, 896), (40, 2048)])
+@pytest.mark.parametrize("rows,d", [(5, 64), (300, 896), (40, 2048), (200, 4096), (96, 5120)])
 @pytest.mark.parametrize("with_extra", [False, True])
 def test_rmsnorm_bwd(ops, ref, rows, d, with_extra):
     nr = rng_floats(1 + d, rows * d, -3, 3).reshape(rows, d)
