@@ -1071,6 +1071,9 @@ class Session {
         }
         return f != 0;
     }
+    // side stream in use for this backward (not while profiling: the per-class event brackets
+    // time kernels one at a time)
+    bool side_on() const { return wgrad_side() && wst && !prof_on; }
     bool lm_tx() const {
         static int f = -1;
         if (f < 0) {
@@ -1450,14 +1453,14 @@ class Session {
     // read that buffer two casts ago); the side stream may read it after this
     uint8_t* quant_grad(const uint16_t* src, int64_t n, int gk_, uint32_t* amax, float* scale) {
         uint8_t* buf = gcodes;
-        if (wgrad_side()) {
+        if (side_on()) {
             buf = gbuf_i ? gcodes2 : gcodes;
             if (wdone_valid[gbuf_i]) QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_wdone[gbuf_i], 0));
         }
         const int h = prof_begin();
         QT_CHECK_K(qtk_quantize_bf16(src, n, gk_, amax, buf, scale, st));
         prof_end(h, 3, 3.0 * n);
-        if (wgrad_side()) {
+        if (side_on()) {
             QT_CHECK_CUDA(cudaEventRecord(ev_qready, st));
             QT_CHECK_CUDA(cudaStreamWaitEvent(wst, ev_qready, 0));
         }
@@ -1475,8 +1478,8 @@ class Session {
         gemm(0, gkind(), kE4M3, true, true, Mo, No, K, gc, lda, act, ldb, gsc, asc, fresh ? EPI_BF16 : EPI_BF16_ACC,
              gbuf(t), No, nullptr,
              0, aseed, t.s_acc, micro_step * (uint64_t)t.numel, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-             0, wgrad_side() ? wst : nullptr);
-        if (wgrad_side()) {
+             0, side_on() ? wst : nullptr);
+        if (side_on()) {
             QT_CHECK_CUDA(cudaEventRecord(ev_wdone[gbuf_i], wst));
             wdone_valid[gbuf_i] = true;
             gbuf_i ^= 1;
@@ -1484,7 +1487,7 @@ class Session {
     }
     // the compute stream waits for every weight gradient issued so far
     void wgrad_join() {
-        if (!wgrad_side()) return;
+        if (!side_on()) return;
         QT_CHECK_CUDA(cudaEventRecord(ev_wjoin, wst));
         QT_CHECK_CUDA(cudaStreamWaitEvent(st, ev_wjoin, 0));
     }
@@ -1583,7 +1586,7 @@ class Session {
             // ---- attention backward + inverse RoPE
             h = prof_begin();
             QT_CHECK_K(qtk_attn_bwd2(b.qkv, b.att32, d_att, d, b.lse, Dv, curB, curT, H, Hkv, hd, q, d_qkv, attn_ws, st,
-                                     attn_two_streams() ? wst : nullptr));
+                                     attn_two_streams() && side_on() ? wst : nullptr));
             prof_end(h, 8, 10.0 * curB * H * (double)curT * curT / 2 * hd);
             h = prof_begin();
             QT_CHECK_K(qtk_rope(d_qkv, M, curT, H + Hkv, hd, q, rope_tab, 1, ga + G_DQKV, st));
