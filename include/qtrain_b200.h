@@ -166,6 +166,8 @@ int qtk_embed_bwd(const int32_t* sorted_pos, const int32_t* seg_off, const int32
 /* attention MMA operand precision: 1 = P (and dS) as bf16 hi + lo (f32-faithful
  * products), 0 = bf16 (default from QTB_ATTN_PLO) */
 void qtk_attn_set_plo(int plo);
+/* attention forward kernel: 1 = two query tiles per CTA (softmax / MMA ping-pong), 0 = one */
+void qtk_attn_set_fwd2q(int on);
 int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
                  float* out32, float* lse, uint32_t* amax, cudaStream_t s);
 /* precision mode (process-wide): fast_exp = __expf for exp(); bwd_split = P and

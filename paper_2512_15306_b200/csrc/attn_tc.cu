@@ -86,6 +86,17 @@ inline cudaEvent_t join_ev() {
     return e;
 }
 
+// forward kernel: 1 = two Q tiles per CTA (fwd2q_tc_kernel), 0 = one (fwd1p_tc_kernel);
+// QTB_ATTN_FWD2Q, qtk_attn_set_fwd2q
+static int g_fwd2q = -1;
+inline int fwd2q_mode() {
+    if (g_fwd2q < 0) {
+        const char* e = getenv("QTB_ATTN_FWD2Q");
+        g_fwd2q = e ? atoi(e) : 0;
+    }
+    return g_fwd2q;
+}
+
 // P (forward) and P / dS (backward) as MMA operands: bf16 hi + lo (16 significant bits,
 // f32-faithful products) or bf16 alone (one MMA per k-step instead of two).
 // QTB_ATTN_PLO=1|0; qtk_attn_set_plo overrides (tests/A-B).
@@ -1504,6 +1515,349 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
     }
 }
 
+
+// ===========================================================================
+// Forward, two Q tiles per CTA (ping-pong).  A CTA owns the adjacent query tiles
+// (2p, 2p+1) of one (head, batch) -- they share every K/V tile but the last --
+// and two softmax warpgroups, one per tile, each thread owning a whole row
+// (no cross-warp max/sum exchange).  S_X = Q_X K_j^T lands in TMEM; the
+// softmax of tile X overwrites its S columns with P (bf16 hi + lo, the
+// backward's chunk map) and the MMA warp accumulates O_X += P_X V_j with P as
+// the TMEM A operand -- no shared-memory round trip for P.  While one tile's
+// softmax runs, the tensor core works on the other tile's S / PV, which is
+// what the one-tile kernel cannot do (its softmax and MMAs serialise).
+// TMEM: S_A [0,128), S_B [128,256), O_A [256,256+HD), O_B [256+HD,256+2HD).
+// Same arithmetic as fwd1p_tc_kernel (online max moved only when it grows by
+// > 2^RESCALE, O rescaled in TMEM then, O / l at the end).
+// ===========================================================================
+template <int HD>
+struct Smem2Q {
+    static constexpr int Q = BQ * HD * 2;
+    static constexpr int K = BKV * HD * 2;
+    static constexpr int V = BKV * HD * 2;
+    static constexpr int OFF_Q = 0;             // tile A at 0, tile B at Q
+    static constexpr int OFF_K = 2 * Q;         // 2 stages
+    static constexpr int OFF_V = OFF_K + 2 * K;  // 2 stages
+    static constexpr int OFF_BAR = OFF_V + 2 * V;
+    static constexpr int BYTES = OFF_BAR + 512 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H,
+                                                         int Hkv, int B, float inv_sqrt_d, uint16_t* __restrict__ out,
+                                                         int64_t ldo, float* __restrict__ out32, float* __restrict__ lse,
+                                                         uint32_t* __restrict__ amax, int plo) {
+    using S = Smem2Q<HD>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + S::OFF_BAR);
+    uint64_t* q_full = bar + 0;
+    uint64_t* q_empty = bar + 1;
+    uint64_t* k_full = bar + 2;    // [2]
+    uint64_t* k_empty = bar + 4;   // [2]
+    uint64_t* v_full = bar + 6;    // [2]
+    uint64_t* v_empty = bar + 8;   // [2]
+    uint64_t* s_full = bar + 10;   // [tile]
+    uint64_t* p_full = bar + 12;   // [tile]
+    uint64_t* pv_done = bar + 14;  // [tile]
+    uint64_t* o_full = bar + 16;   // [tile]
+    uint64_t* o_empty = bar + 18;  // [tile]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 20);
+
+    const int nq = (T + BQ - 1) / BQ;
+    const int npair = (nq + 1) / 2;
+    const int items = npair * H * B;
+    const int d = H * HD;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // longest pairs first: pair p = npair-1 .. 0
+    auto decode = [&](int it, int& pr, int& h, int& b) {
+        pr = npair - 1 - it / (H * B);
+        const int r = it % (H * B);
+        h = r % H;
+        b = r / H;
+    };
+
+    if (warp == 0 && lane == 0) tma_prefetch(&tm);
+    if (warp == 1 && lane == 0) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&k_full[i], 1);
+            mbar_init(&k_empty[i], 1);
+            mbar_init(&v_full[i], 1);
+            mbar_init(&v_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);
+            mbar_init(&pv_done[i], 1);
+            mbar_init(&o_full[i], 1);
+            mbar_init(&o_empty[i], 4);
+        }
+        fence_barrier_init();
+        fence_async_shared();
+    }
+    if (warp == 2) tmem_alloc(tslot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t s_base = smem_u32(sm);
+
+    if (warp == 0 && lane == 0) {
+        // ===== TMA producer: Q_A (+ Q_B), then the K/V tiles the pair needs =====
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        int n_it = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+            int pr, h, b;
+            decode(it, pr, h, b);
+            const int qa = 2 * pr, qb = 2 * pr + 1;
+            const bool hasb = qb < nq;
+            const int nj = hasb ? qb + 1 : qa + 1;
+            const int kvh = h / (H / Hkv);
+            if (n_it > 0) mbar_wait(q_empty, (n_it - 1) & 1);
+            mbar_arrive_expect_tx(q_full, (hasb ? 2 : 1) * S::Q);
+            for (int c = 0; c < HD / 64; ++c) {
+                tma_load_2d(&tm, q_full, sm + S::OFF_Q + c * BQ * 128, h * HD + c * 64, b * T + qa * BQ);
+                if (hasb) tma_load_2d(&tm, q_full, sm + S::OFF_Q + S::Q + c * BQ * 128, h * HD + c * 64, b * T + qb * BQ);
+            }
+            for (int j = 0; j < nj; ++j) {
+                const int krow = b * T + j * BKV;
+                mbar_wait(&k_empty[ks], kph ^ 1);
+                mbar_arrive_expect_tx(&k_full[ks], S::K);
+                for (int c = 0; c < HD / 64; ++c)
+                    tma_load_2d(&tm, &k_full[ks], sm + S::OFF_K + ks * S::K + c * BKV * 128, d + kvh * HD + c * 64, krow);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+                mbar_wait(&v_empty[vs], vph ^ 1);
+                mbar_arrive_expect_tx(&v_full[vs], S::V);
+                for (int c = 0; c < HD / 64; ++c)
+                    tma_load_2d(&tm, &v_full[vs], sm + S::OFF_V + vs * S::V + c * BKV * 128,
+                                d + Hkv * HD + kvh * HD + c * 64, krow);
+                if (++vs == 2) { vs = 0; vph ^= 1; }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer (one elected thread): PV_A(j), S_A(j+1), PV_B(j), S_B(j+1), ... so the
+        // tensor core works on one tile while the other tile's softmax runs =====
+        const uint32_t idesc_s = make_idesc(1, 1, false, false, BQ, BKV);
+        const uint32_t idesc_o = make_idesc(1, 1, false, true, BQ, HD);
+        int ks = 0, vs = 0;
+        uint32_t kph = 0, vph = 0;
+        uint32_t pcnt[2] = {0, 0}, pvcnt[2] = {0, 0}, ocnt[2] = {0, 0};
+        int n_it = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+            int pr, h, b;
+            decode(it, pr, h, b);
+            const int qa = 2 * pr, qb = 2 * pr + 1;
+            const bool hasb = qb < nq;
+            const int nx[2] = {qa + 1, hasb ? qb + 1 : 0};
+            const int nj = hasb ? qb + 1 : qa + 1;
+            const int last = hasb ? 1 : 0;  // the tile whose range is longest: last user of each K tile
+            const int s_total = nx[0] + nx[1];
+            int s_issued = 0;
+            mbar_wait(q_full, n_it & 1);
+            auto s_mma = [&](int x) {
+                const uint32_t ka = s_base + S::OFF_K + ks * S::K;
+                const uint32_t qa_ = s_base + S::OFF_Q + x * S::Q;
+#pragma unroll
+                for (int kk = 0; kk < HD / 16; ++kk)
+                    mma_bf16_ss(tmem + x * 128, kdesc(qa_, kk, BQ * 128), kdesc(ka, kk, BKV * 128), idesc_s, kk > 0);
+                tc_commit(&s_full[x]);
+                if (++s_issued == s_total) tc_commit(q_empty);  // Q no longer read by this item
+            };
+            auto k_release = [&]() {
+                tc_commit(&k_empty[ks]);
+                if (++ks == 2) { ks = 0; kph ^= 1; }
+            };
+            // S(0) of both tiles
+            mbar_wait(&k_full[ks], kph);
+            tc_fence_after();
+            for (int x = 0; x <= last; ++x) s_mma(x);
+            k_release();
+            bool k_ready = false;  // K(j+1) waited for
+            for (int j = 0; j < nj; ++j) {
+                mbar_wait(&v_full[vs], vph);
+                const uint32_t va = s_base + S::OFF_V + vs * S::V;
+                k_ready = false;
+                for (int x = 0; x < 2; ++x) {
+                    if (j >= nx[x]) continue;
+                    mbar_wait(&p_full[x], pcnt[x] & 1);
+                    ++pcnt[x];
+                    if (j == 0 && ocnt[x] > 0) mbar_wait(&o_empty[x], (ocnt[x] - 1) & 1);  // O_X drained
+                    tc_fence_after();
+                    const uint32_t pa = tmem + x * 128;
+                    const uint32_t od = tmem + 256 + x * HD;
+#pragma unroll
+                    for (int kk = 0; kk < BKV / 16; ++kk) {
+                        const uint64_t bd = mndesc(va, kk, BKV * 128);
+                        mma_bf16_ts(od, pa + a_col(kk, 0), bd, idesc_o, (j | kk) != 0);
+                        if (plo) mma_bf16_ts(od, pa + a_col(kk, 1), bd, idesc_o, 1);
+                    }
+                    tc_commit(&pv_done[x]);
+                    ++pvcnt[x];
+                    if (j == nx[x] - 1) {
+                        tc_commit(&o_full[x]);
+                        ++ocnt[x];
+                    }
+                    if (x == last) tc_commit(&v_empty[vs]);  // V(j) read by both tiles' PV
+                    if (j + 1 < nx[x]) {
+                        // S_X(j+1) overwrites the columns PV_X(j) reads as P: wait for it first
+                        if (!k_ready) {
+                            mbar_wait(&k_full[ks], kph);
+                            k_ready = true;
+                        }
+                        mbar_wait(&pv_done[x], (pvcnt[x] - 1) & 1);
+                        tc_fence_after();
+                        s_mma(x);
+                        if (x == last) k_release();
+                    }
+                }
+                if (++vs == 2) { vs = 0; vph ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== softmax: warpgroup x = (warp - 4) / 4 owns tile x; thread = query row =====
+        const int x = (warp - 4) >> 2, wq = warp & 3;
+        const int r = wq * 32 + lane;
+        const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
+        const uint32_t s_cols = lane_base + x * 128;
+        const uint32_t o_cols = lane_base + 256 + x * HD;
+        const float a = inv_sqrt_d * LOG2E;
+        constexpr float RESCALE = 8.0f;
+        uint32_t scnt = 0, ocnt = 0;
+        uint32_t mx = 0;
+        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+            int pr, h, b;
+            decode(it, pr, h, b);
+            const int qt = 2 * pr + x;
+            if (qt >= nq) continue;  // pair without a second tile
+            const int nj = qt + 1;
+            const int q = qt * BQ + r;
+            // l per key half, summed as fwd1p_tc_kernel's two half-row threads do (bitwise equal)
+            float m = -INFINITY, l0 = 0.0f, l1 = 0.0f;
+            for (int j = 0; j < nj; ++j, ++scnt) {
+                mbar_wait(&s_full[x], scnt & 1);
+                tc_fence_after();
+                const bool diag = j == qt;
+                const int kbase = j * BKV;
+                // pass 1: the row max over the tile's 128 keys
+                float mt = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t rr[32];
+                    tmem_ld32(s_cols + c * 32, rr);
+                    tmem_ld_wait();
+                    if (diag) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (kbase + c * 32 + i <= q) mt = fmaxf(mt, __uint_as_float(rr[i]));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) mt = fmaxf(mt, __uint_as_float(rr[i]));
+                    }
+                }
+                const bool grow = mt > m && (m == -INFINITY || (mt - m) * a > RESCALE);
+                if (__any_sync(0xffffffffu, grow && m != -INFINITY)) {
+                    // O_X holds PV(..j-1): complete, since the MMA warp waited for it before S(j)
+                    const float alpha = (grow && m != -INFINITY) ? ex2((m - mt) * a) : 1.0f;
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        uint32_t ov[32];
+                        tmem_ld32(o_cols + c * 32, ov);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+                        tmem_st32(o_cols + c * 32, ov);
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    l0 *= alpha;
+                    l1 *= alpha;
+                }
+                if (grow) m = mt;
+                const float mb = m * a;
+                // pass 2: p = exp2(x a - m a), written over the chunk as bf16 hi (+ lo)
+                float s4[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t rr[32];
+                    tmem_ld32(s_cols + c * 32, rr);
+                    tmem_ld_wait();
+                    float pv[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const bool live = !diag || (kbase + c * 32 + i <= q);
+                        pv[i] = live ? ex2(__fmaf_rn(__uint_as_float(rr[i]), a, -mb)) : 0.0f;
+                    }
+                    const int hh = c >> 1;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        const int il = (c & 1) * 32 + i;  // index within the 64-key half
+                        s4[hh][(il >> 1) & 3] += pv[i] + pv[i + 1];
+                    }
+                    uint32_t hi[16], lo[16];
+                    if (plo) {
+                        split32(pv, hi, lo);
+                        tmem_st16(s_cols + c * 32, hi);
+                        tmem_st16(s_cols + c * 32 + 16, lo);
+                    } else {
+                        round32(pv, hi);
+                        tmem_st16(s_cols + c * 32, hi);
+                    }
+                }
+                l0 += (s4[0][0] + s4[0][1]) + (s4[0][2] + s4[0][3]);
+                l1 += (s4[1][0] + s4[1][1]) + (s4[1][2] + s4[1][3]);
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[x]);
+            }
+            const float l = l0 + l1;
+            const float inv_l = l > 0.0f ? 1.0f / l : 0.0f;
+            mbar_wait(&o_full[x], ocnt & 1);
+            ++ocnt;
+            tc_fence_after();
+            const bool valid = q < T;
+            const int64_t grow_ = (int64_t)b * T + q;
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+                uint32_t rr[32];
+                tmem_ld32(o_cols + c * 32, rr);
+                tmem_ld_wait();
+                if (valid) {
+                    uint4* o16 = reinterpret_cast<uint4*>(out + grow_ * ldo + h * HD + c * 32);
+                    float4* o32 = reinterpret_cast<float4*>(out32 + grow_ * ldo + h * HD + c * 32);
+#pragma unroll
+                    for (int v4 = 0; v4 < 4; ++v4) {
+                        float f[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            f[e] = __uint_as_float(rr[v4 * 8 + e]) * inv_l;
+                            mx = max(mx, abs_bits(bf16r(f[e])));
+                        }
+                        o16[v4] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                                             pack_bf16x2(f[6], f[7]));
+                        if (out32) {
+                            o32[2 * v4] = make_float4(f[0], f[1], f[2], f[3]);
+                            o32[2 * v4 + 1] = make_float4(f[4], f[5], f[6], f[7]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&o_empty[x]);
+            if (valid) lse[((int64_t)b * H + h) * T + q] = m * inv_sqrt_d + logf(l);
+        }
+        mx = warp_max_u32(mx);
+        if (lane == 0 && amax && mx) atomicMax(amax, mx);
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 }  // namespace attn_tc
 }  // namespace qtb
 
@@ -1540,6 +1894,23 @@ extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, in
     if (persistent < 0) {
         const char* e = getenv("QTB_ATTN_PERSIST");
         persistent = e ? atoi(e) : 1;
+    }
+    if (fwd2q_mode() && !two_pass) {  // two Q tiles per CTA, ping-pong softmax / MMA
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int items = (int)ceil_div(ceil_div(T, BQ), 2) * H * B;
+        const unsigned pg = (unsigned)std::min(items, sms);
+#define QTB_FWD2Q(HDV)                                                                                           \
+        {                                                                                                          \
+            const int smem = Smem2Q<HDV>::BYTES;                                                                   \
+            cudaFuncSetAttribute(fwd2q_tc_kernel<HDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
+            fwd2q_tc_kernel<HDV><<<pg, NT, smem, s>>>(tm, T, H, Hkv, B, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, \
+                                                      amax, p_lo_mode());                                          \
+        }
+        if (hd == 64) QTB_FWD2Q(64) else QTB_FWD2Q(128)
+#undef QTB_FWD2Q
+        return (int)cudaGetLastError();
     }
     if (persistent && !two_pass) {
         int dev = 0, sms = 148;
@@ -1635,3 +2006,4 @@ extern "C" int qtk_attn_bwd_tc2(const void* qkv, const float* out32, const void*
 }
 
 extern "C" void qtk_attn_set_plo(int plo) { qtb::attn_tc::g_plo = plo; }
+extern "C" void qtk_attn_set_fwd2q(int on) { qtb::attn_tc::g_fwd2q = on; }
