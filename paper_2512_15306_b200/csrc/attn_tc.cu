@@ -92,7 +92,7 @@ static int g_fwd2q = -1;
 inline int fwd2q_mode() {
     if (g_fwd2q < 0) {
         const char* e = getenv("QTB_ATTN_FWD2Q");
-        g_fwd2q = e ? atoi(e) : 0;
+        g_fwd2q = e ? atoi(e) : 1;
     }
     return g_fwd2q;
 }

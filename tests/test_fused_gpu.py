@@ -252,3 +252,27 @@ def test_ce_stats_epilogue_matches_two_pass(ops, N, d, V):
     full1 = hi1.float() + lo1.float()
     full2 = hi2.float() + lo2.float()
     assert torch.allclose(full1, full2, rtol=5e-5, atol=1e-12)
+
+
+@pytest.mark.parametrize("B,T,H,Hkv,hd", [(2, 256, 4, 2, 64), (1, 384, 4, 1, 64), (2, 200, 4, 4, 128),
+                                          (4, 1024, 14, 2, 64), (2, 1024, 32, 32, 128), (3, 640, 8, 2, 128)])
+def test_attention_fwd_two_tile_kernel_bitwise_equals_one_tile(ops, B, T, H, Hkv, hd):
+    """fwd2q_tc_kernel (two query tiles per CTA, P through TMEM) reproduces fwd1p_tc_kernel
+    bit for bit (out, unrounded out32, LSE, absmax): same P operands, same PV issue order,
+    l summed per key half as the one-tile kernel's two half-row threads do.  Odd tile
+    counts and ragged T included."""
+    from paper_2512_15306_b200 import _lib
+    L = _lib.lib()
+    d = H * hd
+    q = d + 2 * Hkv * hd
+    g = torch.Generator(device="cuda").manual_seed(T + hd)
+    qkv = (torch.randn(B * T, q, device="cuda", generator=g) * 1.5).to(torch.bfloat16)
+    res = []
+    try:
+        for mode in (0, 1):
+            L.qtk_attn_set_fwd2q(mode)
+            res.append(ops.attn_fwd(qkv, B, T, H, Hkv, hd))
+    finally:
+        L.qtk_attn_set_fwd2q(1)
+    for a, b in zip(*res):
+        assert torch.equal(a, b)
