@@ -1602,6 +1602,7 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
     const uint32_t tmem = *tslot;
     const uint32_t s_base = smem_u32(sm);
 
+    if (warp < 4) setmaxnreg_dec<96>();  // producer / MMA / idle warpgroup
     if (warp == 0 && lane == 0) {
         // ===== TMA producer: Q_A (+ Q_B), then the K/V tiles the pair needs =====
         int ks = 0, vs = 0;
@@ -1678,6 +1679,7 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
                 mbar_wait(&v_full[vs], vph);
                 const uint32_t va = s_base + S::OFF_V + vs * S::V;
                 k_ready = false;
+#pragma unroll
                 for (int x = 0; x < 2; ++x) {
                     if (j >= nx[x]) continue;
                     mbar_wait(&p_full[x], pcnt[x] & 1);
@@ -1716,6 +1718,9 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
         }
     } else if (warp >= 4) {
         // ===== softmax: warpgroup x = (warp - 4) / 4 owns tile x; thread = query row =====
+        // 200 registers (the producer warpgroup gave its surplus back): the row's 128 scores
+        // come out of TMEM in one round trip and stay in registers for the max and exp passes
+        setmaxnreg_inc<200>();
         const int x = (warp - 4) >> 2, wq = warp & 3;
         const int r = wq * 32 + lane;
         const uint32_t lane_base = tmem + ((uint32_t)(wq * 32) << 16);
@@ -1737,29 +1742,31 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
             for (int j = 0; j < nj; ++j, ++scnt) {
                 mbar_wait(&s_full[x], scnt & 1);
                 tc_fence_after();
-                const bool diag = j == qt;
-                const int kbase = j * BKV;
+                uint32_t rr[4][32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(s_cols + c * 32, rr[c]);
+                tmem_ld_wait();
+                if (j == qt) {
+                    // causal diagonal tile: keys past the row's query become -inf (max unaffected,
+                    // exp2 -> +0, exactly the masked value of the one-tile kernel)
+                    const int lim = q - j * BKV;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (c * 32 + i > lim) rr[c][i] = 0xff800000u;
+                }
                 // pass 1: the row max over the tile's 128 keys
                 float mt = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t rr[32];
-                    tmem_ld32(s_cols + c * 32, rr);
-                    tmem_ld_wait();
-                    if (diag) {
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (kbase + c * 32 + i <= q) mt = fmaxf(mt, __uint_as_float(rr[i]));
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) mt = fmaxf(mt, __uint_as_float(rr[i]));
-                    }
-                }
+                    for (int i = 0; i < 32; ++i) mt = fmaxf(mt, __uint_as_float(rr[c][i]));
                 const bool grow = mt > m && (m == -INFINITY || (mt - m) * a > RESCALE);
                 if (__any_sync(0xffffffffu, grow && m != -INFINITY)) {
                     // O_X holds PV(..j-1): complete, since the MMA warp waited for it before S(j)
                     const float alpha = (grow && m != -INFINITY) ? ex2((m - mt) * a) : 1.0f;
-#pragma unroll
+#pragma unroll 1
                     for (int c = 0; c < HD / 32; ++c) {
                         uint32_t ov[32];
                         tmem_ld32(o_cols + c * 32, ov);
@@ -1773,20 +1780,14 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
                     l1 *= alpha;
                 }
                 if (grow) m = mt;
-                const float mb = m * a;
+                const float nmb = -(m * a);
                 // pass 2: p = exp2(x a - m a), written over the chunk as bf16 hi (+ lo)
                 float s4[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
-                    uint32_t rr[32];
-                    tmem_ld32(s_cols + c * 32, rr);
-                    tmem_ld_wait();
                     float pv[32];
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        const bool live = !diag || (kbase + c * 32 + i <= q);
-                        pv[i] = live ? ex2(__fmaf_rn(__uint_as_float(rr[i]), a, -mb)) : 0.0f;
-                    }
+                    for (int i = 0; i < 32; ++i) pv[i] = ex2(__fmaf_rn(__uint_as_float(rr[c][i]), a, nmb));
                     const int hh = c >> 1;
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {

@@ -1,3 +1,4 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:"fwd2q|dkdv|dq_tc" --launch-skip 3 -c 3 -o gpurun_out/attn05 -f python scripts/attn_prof.py 0.5b > gpurun_out/ncu_attn.log 2>&1; echo "ncu rc=$?"; tail -5 gpurun_out/ncu_attn.log
+timeout 300 python scripts/attn_fwd2q.py > gpurun_out/fwd2q.log 2>&1; echo "fwd2q rc=$?"; cat gpurun_out/fwd2q.log | tail -12
+timeout 600 python -m pytest tests/test_fused_gpu.py -x -q -k "attention" > gpurun_out/a1.log 2>&1; echo "attn rc=$?"; tail -3 gpurun_out/a1.log
