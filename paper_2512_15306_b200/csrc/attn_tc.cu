@@ -989,6 +989,12 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
         "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
 }
+// one 32-byte global store (sm_100 256-bit STG); p 32-byte aligned
+__device__ __forceinline__ void st_global_v8(void* p, const uint32_t* v) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // A operand from TMEM
 // TMEM column of the bf16 A operand for k-step kk (16 k values) of a 128-wide
@@ -1546,7 +1552,7 @@ template <int HD>
 __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__ CUtensorMap tm, int T, int H,
                                                          int Hkv, int B, float inv_sqrt_d, uint16_t* __restrict__ out,
                                                          int64_t ldo, float* __restrict__ out32, float* __restrict__ lse,
-                                                         uint32_t* __restrict__ amax, int plo) {
+                                                         uint32_t* __restrict__ amax, int plo, int v8) {
     using S = Smem2Q<HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1569,7 +1575,12 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
     const int items = npair * H * B;
     const int d = H * HD;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // longest pairs first: pair p = npair-1 .. 0
+    // longest pairs first: pair p = npair-1 .. 0, dealt to the CTAs in snake order
+    // (round k runs CTA 0..G-1 when even, G-1..0 when odd) so no CTA collects the
+    // longest item of every round
+    auto snake = [&](int k) {
+        return k * (int)gridDim.x + ((k & 1) ? (int)gridDim.x - 1 - (int)blockIdx.x : (int)blockIdx.x);
+    };
     auto decode = [&](int it, int& pr, int& h, int& b) {
         pr = npair - 1 - it / (H * B);
         const int r = it % (H * B);
@@ -1608,7 +1619,9 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
         int ks = 0, vs = 0;
         uint32_t kph = 0, vph = 0;
         int n_it = 0;
-        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+        for (int k = 0;; ++k, ++n_it) {
+            const int it = snake(k);
+            if (it >= items) break;
             int pr, h, b;
             decode(it, pr, h, b);
             const int qa = 2 * pr, qb = 2 * pr + 1;
@@ -1645,7 +1658,9 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
         uint32_t kph = 0, vph = 0;
         uint32_t pcnt[2] = {0, 0}, pvcnt[2] = {0, 0}, ocnt[2] = {0, 0};
         int n_it = 0;
-        for (int it = blockIdx.x; it < items; it += gridDim.x, ++n_it) {
+        for (int k = 0;; ++k, ++n_it) {
+            const int it = snake(k);
+            if (it >= items) break;
             int pr, h, b;
             decode(it, pr, h, b);
             const int qa = 2 * pr, qb = 2 * pr + 1;
@@ -1730,7 +1745,9 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
         constexpr float RESCALE = 8.0f;
         uint32_t scnt = 0, ocnt = 0;
         uint32_t mx = 0;
-        for (int it = blockIdx.x; it < items; it += gridDim.x) {
+        for (int k = 0;; ++k) {
+            const int it = snake(k);
+            if (it >= items) break;
             int pr, h, b;
             decode(it, pr, h, b);
             const int qt = 2 * pr + x;
@@ -1818,34 +1835,49 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
             tc_fence_after();
             const bool valid = q < T;
             const int64_t grow_ = (int64_t)b * T + q;
+            // O_X leaves TMEM in one round trip; the MMA warp may refill it while we store
+            uint32_t ro[HD / 32][32];
 #pragma unroll
-            for (int c = 0; c < HD / 32; ++c) {
-                uint32_t rr[32];
-                tmem_ld32(o_cols + c * 32, rr);
-                tmem_ld_wait();
-                if (valid) {
-                    uint4* o16 = reinterpret_cast<uint4*>(out + grow_ * ldo + h * HD + c * 32);
-                    float4* o32 = reinterpret_cast<float4*>(out32 + grow_ * ldo + h * HD + c * 32);
+            for (int c = 0; c < HD / 32; ++c) tmem_ld32(o_cols + c * 32, ro[c]);
+            tmem_ld_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&o_empty[x]);
+            if (valid) {
 #pragma unroll
-                    for (int v4 = 0; v4 < 4; ++v4) {
-                        float f[8];
+                for (int c = 0; c < HD / 32; ++c) {
+                    float f[32];
+                    uint32_t pk[16];
 #pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            f[e] = __uint_as_float(rr[v4 * 8 + e]) * inv_l;
-                            mx = max(mx, abs_bits(bf16r(f[e])));
-                        }
-                        o16[v4] = make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
-                                             pack_bf16x2(f[6], f[7]));
-                        if (out32) {
-                            o32[2 * v4] = make_float4(f[0], f[1], f[2], f[3]);
-                            o32[2 * v4 + 1] = make_float4(f[4], f[5], f[6], f[7]);
+                    for (int e = 0; e < 32; ++e) {
+                        f[e] = __uint_as_float(ro[c][e]) * inv_l;
+                        mx = max(mx, abs_bits(bf16r(f[e])));
+                    }
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) pk[e] = pack_bf16x2(f[2 * e], f[2 * e + 1]);
+                    uint16_t* o16 = out + grow_ * ldo + h * HD + c * 32;
+                    float* o32 = out32 ? out32 + grow_ * ldo + h * HD + c * 32 : nullptr;
+                    if (v8) {  // 32-byte stores: whole sectors per thread-row
+                        st_global_v8(o16, pk);
+                        st_global_v8(o16 + 16, pk + 8);
+                        if (o32)
+#pragma unroll
+                            for (int v = 0; v < 4; ++v) st_global_v8(o32 + 8 * v, reinterpret_cast<const uint32_t*>(f) + 8 * v);
+                    } else {
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) {
+                            reinterpret_cast<uint4*>(o16)[v] =
+                                make_uint4(pk[4 * v], pk[4 * v + 1], pk[4 * v + 2], pk[4 * v + 3]);
+                            if (o32) {
+                                reinterpret_cast<float4*>(o32)[2 * v] =
+                                    make_float4(f[8 * v], f[8 * v + 1], f[8 * v + 2], f[8 * v + 3]);
+                                reinterpret_cast<float4*>(o32)[2 * v + 1] =
+                                    make_float4(f[8 * v + 4], f[8 * v + 5], f[8 * v + 6], f[8 * v + 7]);
+                            }
                         }
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&o_empty[x]);
             if (valid) lse[((int64_t)b * H + h) * T + q] = m * inv_sqrt_d + logf(l);
         }
         mx = warp_max_u32(mx);
@@ -1902,12 +1934,13 @@ extern "C" int qtk_attn_fwd_tc(const void* qkv, int B, int T, int H, int Hkv, in
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int items = (int)ceil_div(ceil_div(T, BQ), 2) * H * B;
         const unsigned pg = (unsigned)std::min(items, sms);
+        const int v8 = ((((uintptr_t)out) | ((uintptr_t)out32)) & 31) == 0 && ldo % 16 == 0;
 #define QTB_FWD2Q(HDV)                                                                                           \
         {                                                                                                          \
             const int smem = Smem2Q<HDV>::BYTES;                                                                   \
             cudaFuncSetAttribute(fwd2q_tc_kernel<HDV>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);         \
             fwd2q_tc_kernel<HDV><<<pg, NT, smem, s>>>(tm, T, H, Hkv, B, inv_sqrt_d, (uint16_t*)out, ldo, out32, lse, \
-                                                      amax, p_lo_mode());                                          \
+                                                      amax, p_lo_mode(), v8);                                      \
         }
         if (hd == 64) QTB_FWD2Q(64) else QTB_FWD2Q(128)
 #undef QTB_FWD2Q
