@@ -168,6 +168,9 @@ int qtk_embed_bwd(const int32_t* sorted_pos, const int32_t* seg_off, const int32
 void qtk_attn_set_plo(int plo);
 /* attention forward kernel: 1 = two query tiles per CTA (softmax / MMA ping-pong), 0 = one */
 void qtk_attn_set_fwd2q(int on);
+/* RMSNorm path: 0 by shape, 1 split-role chain kernel on the streaming path, 2 split-role chain + row
+ * kernels everywhere, 3 (default) forward as 2 and backward as 1; all bit-identical outputs */
+void qtk_rms_set_path(int mode);
 int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
                  float* out32, float* lse, uint32_t* amax, cudaStream_t s);
 /* precision mode (process-wide): fast_exp = __expf for exp(); bwd_split = P and

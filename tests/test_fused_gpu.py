@@ -276,3 +276,37 @@ def test_attention_fwd_two_tile_kernel_bitwise_equals_one_tile(ops, B, T, H, Hkv
         L.qtk_attn_set_fwd2q(1)
     for a, b in zip(*res):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("rows,d,resid", [(16384, 896, True), (200, 896, True), (8192, 4096, True), (300, 4096, False),
+                                          (77, 5120, True), (1000, 1536, True)])
+def test_rmsnorm_split_role_chain_bitwise(ops, rows, d, resid):
+    """rms_chain2_kernel (producer warps form the terms, one chain lane per row adds them)
+    gives the same inv / normed / nr / d_in / absmax as the fused single-pass kernels and the
+    one-role chain kernel: the same f32 operations in the same order (dgamma: same partials
+    only when both runs take the chain + rows path; against the fused path's coarser partials
+    it is a regrouped sum, compared within 2e-4)."""
+    from paper_2512_15306_b200 import _lib
+    L = _lib.lib()
+    g = torch.Generator(device="cuda").manual_seed(rows + d)
+    bf = lambda *s: (torch.randn(*s, device="cuda", generator=g) * 0.7).to(torch.bfloat16)
+    x, res, dy, ex, gam = bf(rows, d), bf(rows, d), bf(rows, d), bf(rows, d), bf(d) + 1
+    outs = []
+    try:
+        for mode in (0, 1, 2, 3):
+            L.qtk_rms_set_path(mode)
+            nr, normed, s1 = ops.rmsnorm_fwd(x if resid else None, res, gam)
+            din, dg, s2 = ops.rmsnorm_bwd(nr if resid else res, gam, dy, ex)
+            torch.cuda.synchronize()
+            outs.append((nr, normed, s1, din, s2, dg))
+    finally:
+        L.qtk_rms_set_path(3)
+    for mode, o in ((1, outs[1]), (2, outs[2]), (3, outs[3])):
+        for k in range(5):
+            if outs[0][k] is None:
+                continue
+            assert torch.equal(outs[0][k], o[k]), (mode, k)
+        if mode in (1, 3):  # same backward path (and dgamma partials) as mode 0
+            assert torch.equal(o[5], outs[0][5])
+        else:  # fused partials (R rows) vs 16-row partials: same sums, regrouped
+            torch.testing.assert_close(o[5], outs[0][5], rtol=2e-4, atol=1e-6)
