@@ -1008,13 +1008,41 @@ __device__ __forceinline__ uint32_t cvt_bf16x2(float lo, float hi) {
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
     return r;
 }
+// sm_100 paired f32 arithmetic (FFMA2 / FMUL2 / FADD2): each lane is the IEEE
+// round-to-nearest scalar operation, so results are bit-identical to fma / mul / sub
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    float2 r;
+    asm("{\n\t.reg .b64 a, b, c, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+        "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+    return r;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    float2 r;
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    float2 r;
+    asm("{\n\t.reg .b64 a, b, d;\n\tmov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "sub.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(r.x), "=f"(r.y)
+        : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+    return r;
+}
 // v -> bf16 hi + bf16 lo (v - hi), packed pairs; hi is v rounded to nearest
 __device__ __forceinline__ void split32(const float (&v)[32], uint32_t (&hi)[16], uint32_t (&lo)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
         const uint32_t h = cvt_bf16x2(v[2 * i], v[2 * i + 1]);
         hi[i] = h;
-        lo[i] = cvt_bf16x2(v[2 * i] - __uint_as_float(h << 16), v[2 * i + 1] - __uint_as_float(h & 0xffff0000u));
+        const float2 d = sub2(make_float2(v[2 * i], v[2 * i + 1]),
+                              make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xffff0000u)));
+        lo[i] = cvt_bf16x2(d.x, d.y);
     }
 }
 // v -> bf16 (round to nearest), packed pairs: the single-part operand of the bf16 P / dS mode
@@ -1041,11 +1069,21 @@ __device__ __forceinline__ void dkdv_elem(const uint32_t (&rs)[32], const uint32
         const float4 d4 = lds4(sLD + 128 + 4 * i);
         const float nl[4] = {l4.x, l4.y, l4.z, l4.w}, dd[4] = {d4.x, d4.y, d4.z, d4.w};
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            float p = ex2(__fmaf_rn(__uint_as_float(rs[i + u]), c_s, nl[u]));
-            if (MASK) p = qrel + i + u >= 0 ? p : 0.0f;
-            pv[i + u] = p;
-            dsv[i + u] = p * __fmaf_rn(__uint_as_float(rp[i + u]), inv_sqrt_d, -dd[u]);
+        for (int u = 0; u < 4; u += 2) {
+            const float2 e = fma2(make_float2(__uint_as_float(rs[i + u]), __uint_as_float(rs[i + u + 1])),
+                                  make_float2(c_s, c_s), make_float2(nl[u], nl[u + 1]));
+            float p0 = ex2(e.x), p1 = ex2(e.y);
+            if (MASK) {
+                p0 = qrel + i + u >= 0 ? p0 : 0.0f;
+                p1 = qrel + i + u + 1 >= 0 ? p1 : 0.0f;
+            }
+            pv[i + u] = p0;
+            pv[i + u + 1] = p1;
+            const float2 dp = fma2(make_float2(__uint_as_float(rp[i + u]), __uint_as_float(rp[i + u + 1])),
+                                   make_float2(inv_sqrt_d, inv_sqrt_d), make_float2(-dd[u], -dd[u + 1]));
+            const float2 ds = mul2(make_float2(p0, p1), dp);
+            dsv[i + u] = ds.x;
+            dsv[i + u + 1] = ds.y;
         }
     }
 }
@@ -1054,10 +1092,19 @@ template <bool MASK>
 __device__ __forceinline__ void dq_elem(const uint32_t (&rs)[32], const uint32_t (&rp)[32], float c_s, float nl,
                                         float inv_sqrt_d, float dsc, int k0, int lim, float (&dsv)[32]) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-        float p = ex2(__fmaf_rn(__uint_as_float(rs[i]), c_s, nl));
-        if (MASK) p = k0 + i <= lim ? p : 0.0f;
-        dsv[i] = p * __fmaf_rn(__uint_as_float(rp[i]), inv_sqrt_d, -dsc);
+    for (int i = 0; i < 32; i += 2) {
+        const float2 e = fma2(make_float2(__uint_as_float(rs[i]), __uint_as_float(rs[i + 1])), make_float2(c_s, c_s),
+                              make_float2(nl, nl));
+        float p0 = ex2(e.x), p1 = ex2(e.y);
+        if (MASK) {
+            p0 = k0 + i <= lim ? p0 : 0.0f;
+            p1 = k0 + i + 1 <= lim ? p1 : 0.0f;
+        }
+        const float2 dp = fma2(make_float2(__uint_as_float(rp[i]), __uint_as_float(rp[i + 1])),
+                               make_float2(inv_sqrt_d, inv_sqrt_d), make_float2(-dsc, -dsc));
+        const float2 ds = mul2(make_float2(p0, p1), dp);
+        dsv[i] = ds.x;
+        dsv[i + 1] = ds.y;
     }
 }
 
