@@ -356,7 +356,8 @@ def main():
         roof["algorithmic_bytes_per_launch"] = fp8_gemm_bytes_per_step(cfg, B * T) / max(dom["launches"], 1)
     # DRAM bytes per launch of the dominant class from the committed ncu capture of one step
     # (scripts/traffic_summary.py; cold-cache serialised replay), when it matches this config
-    tf = ROOT / "profiles" / "r01_traffic_0.5b.json"
+    tf = next((ROOT / "profiles" / f"r{r:02d}_traffic_0.5b.json" for r in (2, 1)
+               if (ROOT / "profiles" / f"r{r:02d}_traffic_0.5b.json").exists()), ROOT / "profiles" / "r01_traffic_0.5b.json")
     if args.config == "qwen2.5-0.5b" and B == 16 and tf.exists():
         try:
             t = json.loads(tf.read_text())["classes"].get(dom_name)

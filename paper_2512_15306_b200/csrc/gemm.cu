@@ -974,6 +974,11 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     const int tiles = p.num_m * p.num_n;
     const int splits = dec.splits;
     p.splits = splits;
+    // L2-aware order: when an M panel is shared by few N tiles, run those N tiles side by side
+    // (split-K too: the LM-head dgrad's 4 N tiles then share each dlogits panel in L2 instead
+    // of re-streaming it once per N tile, 20.3 -> 15.6 GB per launch; with hundreds of M
+    // panels -- the LM-head wgrad, M = vocab -- the M-fast order measured better, 13.1 vs 15.9 GB)
+    p.n_fast = p.num_n <= p.num_m && (splits == 1 || p.num_m <= 256);
     p.kb_per_split = (int)ceil_div(p.num_k, splits);
     if (splits > 1) {
         p.splits = (int)ceil_div(p.num_k, p.kb_per_split);  // no empty splits (== splits, see decide)
@@ -992,8 +997,6 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
                                                 g->sr_stream, g->sr_base, g->sr_micro_step);
         return (int)cudaGetLastError();
     }
-    // L2-aware order: when an M panel is shared by few N tiles, run those N tiles side by side
-    p.n_fast = p.num_n <= p.num_m;
     // staged TMA-store epilogue: 16-B aligned output (and residual) rows
     {
         const int oel = g->epi == EPI_F32 ? 4 : 2;
