@@ -21,7 +21,10 @@ def shapes():
                 (tag, "dgrad_down", M, Hh, d, 0, 1, EPI_BF16), (tag, "dgrad_gu", M, d, F, 0, 1, EPI_BF16),
                 (tag, "dgrad_o", M, d, d, 0, 1, EPI_BF16), (tag, "dgrad_qkv", M, d, q, 0, 1, EPI_BF16),
                 (tag, "wgrad_down", d, Hh, M, 1, 1, EPI_ACC), (tag, "wgrad_gu", F, d, M, 1, 1, EPI_ACC),
-                (tag, "wgrad_o", d, d, M, 1, 1, EPI_ACC), (tag, "wgrad_qkv", q, d, M, 1, 1, EPI_ACC)]
+                (tag, "wgrad_o", d, d, M, 1, 1, EPI_ACC), (tag, "wgrad_qkv", q, d, M, 1, 1, EPI_ACC),
+                # first micro-step of an accumulation (GA = 1: every step): fresh bf16 epilogue
+                (tag, "wgradF_down", d, Hh, M, 1, 1, EPI_BF16), (tag, "wgradF_gu", F, d, M, 1, 1, EPI_BF16),
+                (tag, "wgradF_o", d, d, M, 1, 1, EPI_BF16), (tag, "wgradF_qkv", q, d, M, 1, 1, EPI_BF16)]
     return out
 
 
@@ -46,11 +49,11 @@ def child():
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-                for _ in range(10):
+                for _ in range(20):
                     f()
                 e1.record()
                 torch.cuda.synchronize()
-                us = e0.elapsed_time(e1) / 10 * 1e3
+                us = e0.elapsed_time(e1) / 20 * 1e3
             except Exception as e:  # noqa: BLE001
                 plan, us = {"error": str(e)[:80]}, None
             res.append({"shape": f"{tag}/{name}", "bn_req": bn, "plan": plan, "us": us,
