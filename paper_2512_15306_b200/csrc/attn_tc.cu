@@ -1108,6 +1108,133 @@ __device__ __forceinline__ void dq_elem(const uint32_t (&rs)[32], const uint32_t
     }
 }
 
+// Batched MMA issue.  The attention MMAs are short (M128 x N64 x K16 = 32 tensor
+// cycles), and issuing each through its own elect / uniform-register conversion costs
+// more than that, so the MMA warp became the critical path of the backward.  These
+// issue a whole group from one elect with the per-k-step operand offsets added inside
+// the asm (same MMAs, same order as the per-call loops they replace).
+#define QTB_TS(D, A, B, ID, P) "@E tcgen05.mma.cta_group::1.kind::f16 [" D "], [" A "], " B ", " ID ", " P ";\n\t"
+#define QTB_SS(D, A, B, ID, P) "@E tcgen05.mma.cta_group::1.kind::f16 [" D "], " A ", " B ", " ID ", " P ";\n\t"
+// dV += P^T dO_sub (hi, lo) and dK += dS^T Q_sub (hi, lo) for the 4 k-steps of a 64-query
+// sub-tile: A columns a_col(kk, part) of pb (P) / pb + 64 (dS), B = MN-major descriptors
+// advancing 16 rows (2048 B) per k-step; acc: accumulate flag of the first k-step.
+// operands: %0 dv, %1 dk, %2 pb, %3 bo, %4 bq, %5 idesc, %6 acc
+#define QTB_G(DV_A, DK_A, B1, B2) \
+    "add.u32 a, %2, " #DV_A ";\n\t" QTB_TS("%0", "a", B1, "%5", "T") \
+    "add.u32 a, %2, " #DK_A ";\n\t" QTB_TS("%1", "a", B2, "%5", "T")
+__device__ __forceinline__ void mma_g4_hilo(uint32_t dv, uint32_t dk, uint32_t pb, uint64_t bo, uint64_t bq,
+                                            uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred E, p, T;\n\t.reg .b32 a;\n\t.reg .b64 o, q;\n\t"
+        "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 T, %6, %6;\n\t"
+        QTB_TS("%0", "%2", "%3", "%5", "p")
+        "add.u32 a, %2, 16;\n\t" QTB_TS("%0", "a", "%3", "%5", "T")
+        "add.u32 a, %2, 64;\n\t" QTB_TS("%1", "a", "%4", "%5", "p")
+        "add.u32 a, %2, 80;\n\t" QTB_TS("%1", "a", "%4", "%5", "T")
+        "add.u64 o, %3, 128;\n\tadd.u64 q, %4, 128;\n\t"
+        "add.u32 a, %2, 8;\n\t" QTB_TS("%0", "a", "o", "%5", "T")
+        "add.u32 a, %2, 24;\n\t" QTB_TS("%0", "a", "o", "%5", "T")
+        "add.u32 a, %2, 72;\n\t" QTB_TS("%1", "a", "q", "%5", "T")
+        "add.u32 a, %2, 88;\n\t" QTB_TS("%1", "a", "q", "%5", "T")
+        "add.u64 o, %3, 256;\n\tadd.u64 q, %4, 256;\n\t"
+        "add.u32 a, %2, 32;\n\t" QTB_TS("%0", "a", "o", "%5", "T")
+        "add.u32 a, %2, 48;\n\t" QTB_TS("%0", "a", "o", "%5", "T")
+        "add.u32 a, %2, 96;\n\t" QTB_TS("%1", "a", "q", "%5", "T")
+        "add.u32 a, %2, 112;\n\t" QTB_TS("%1", "a", "q", "%5", "T")
+        "add.u64 o, %3, 384;\n\tadd.u64 q, %4, 384;\n\t"
+        "add.u32 a, %2, 40;\n\t" QTB_TS("%0", "a", "o", "%5", "T")
+        "add.u32 a, %2, 56;\n\t" QTB_TS("%0", "a", "o", "%5", "T")
+        "add.u32 a, %2, 104;\n\t" QTB_TS("%1", "a", "q", "%5", "T")
+        "add.u32 a, %2, 120;\n\t" QTB_TS("%1", "a", "q", "%5", "T")
+        "}" ::"r"(dv), "r"(dk), "r"(pb), "l"(bo), "l"(bq), "r"(idesc), "r"(acc)
+        : "memory");
+}
+#undef QTB_G
+// dQ += dS K_sub (hi, lo) for the 4 k-steps of a 64-key sub-tile
+// operands: %0 dq, %1 pb, %2 bk, %3 idesc, %4 acc
+__device__ __forceinline__ void mma_dq4_hilo(uint32_t dq, uint32_t pb, uint64_t bk, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred E, p, T;\n\t.reg .b32 a;\n\t.reg .b64 q;\n\t"
+        "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 T, %4, %4;\n\t"
+        QTB_TS("%0", "%1", "%2", "%3", "p")
+        "add.u32 a, %1, 16;\n\t" QTB_TS("%0", "a", "%2", "%3", "T")
+        "add.u64 q, %2, 128;\n\t"
+        "add.u32 a, %1, 8;\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+        "add.u32 a, %1, 24;\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+        "add.u64 q, %2, 256;\n\t"
+        "add.u32 a, %1, 32;\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+        "add.u32 a, %1, 48;\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+        "add.u64 q, %2, 384;\n\t"
+        "add.u32 a, %1, 40;\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+        "add.u32 a, %1, 56;\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+        "}" ::"r"(dq), "r"(pb), "l"(bk), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// two SS products over HD/16 k-steps (S = X Y^T and dP = U W^T sharing the k loop): K-major
+// SW128 descriptors advance 32 B (2 units) per k-step inside a 64-column atom, atom_stride >> 4
+// (1024 units) across.  operands: %0 d0, %1 a0, %2 b0, %3 d1, %4 a1, %5 b1, %6 idesc
+#define QTB_SS_STEP(OFF, P)                                                                      \
+    "add.u64 x, %1, " #OFF ";\n\tadd.u64 y, %2, " #OFF ";\n\t" QTB_SS("%0", "x", "y", "%6", P) \
+    "add.u64 x, %4, " #OFF ";\n\tadd.u64 y, %5, " #OFF ";\n\t" QTB_SS("%3", "x", "y", "%6", P)
+template <int HD>
+__device__ __forceinline__ void mma_ss2(uint32_t d0, uint64_t a0, uint64_t b0, uint32_t d1, uint64_t a1, uint64_t b1,
+                                        uint32_t idesc) {
+    static_assert(HD == 64 || HD == 128, "head dim");
+    if constexpr (HD == 64) {
+        asm volatile("{\n\t.reg .pred E, F, T;\n\t.reg .b64 x, y;\n\t"
+                     "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 F, %6, %6;\n\tsetp.eq.b32 T, %6, %6;\n\t"
+                     QTB_SS_STEP(0, "F") QTB_SS_STEP(2, "T") QTB_SS_STEP(4, "T") QTB_SS_STEP(6, "T")
+                     "}" ::"r"(d0), "l"(a0), "l"(b0), "r"(d1), "l"(a1), "l"(b1), "r"(idesc)
+                     : "memory");
+    } else {
+        asm volatile("{\n\t.reg .pred E, F, T;\n\t.reg .b64 x, y;\n\t"
+                     "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 F, %6, %6;\n\tsetp.eq.b32 T, %6, %6;\n\t"
+                     QTB_SS_STEP(0, "F") QTB_SS_STEP(2, "T") QTB_SS_STEP(4, "T") QTB_SS_STEP(6, "T")
+                     QTB_SS_STEP(1024, "T") QTB_SS_STEP(1026, "T") QTB_SS_STEP(1028, "T") QTB_SS_STEP(1030, "T")
+                     "}" ::"r"(d0), "l"(a0), "l"(b0), "r"(d1), "l"(a1), "l"(b1), "r"(idesc)
+                     : "memory");
+    }
+}
+#undef QTB_SS_STEP
+// O += P V (hi, lo) over the 8 k-steps of a 128-key tile (forward PV, P from TMEM with the
+// a_col chunk map).  operands: %0 o, %1 pa, %2 bv, %3 idesc, %4 acc
+#define QTB_PV(OFF_HI, OFF_LO, BOFF)                                                          \
+    "add.u64 q, %2, " #BOFF ";\n\t"                                                           \
+    "add.u32 a, %1, " #OFF_HI ";\n\t" QTB_TS("%0", "a", "q", "%3", "T")                        \
+    "add.u32 a, %1, " #OFF_LO ";\n\t" QTB_TS("%0", "a", "q", "%3", "T")
+__device__ __forceinline__ void mma_pv8_hilo(uint32_t o, uint32_t pa, uint64_t bv, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred E, p, T;\n\t.reg .b32 a;\n\t.reg .b64 q;\n\t"
+        "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.b32 T, %4, %4;\n\t"
+        QTB_TS("%0", "%1", "%2", "%3", "p")
+        "add.u32 a, %1, 16;\n\t" QTB_TS("%0", "a", "%2", "%3", "T")
+        QTB_PV(8, 24, 128) QTB_PV(32, 48, 256) QTB_PV(40, 56, 384) QTB_PV(64, 80, 512) QTB_PV(72, 88, 640)
+        QTB_PV(96, 112, 768) QTB_PV(104, 120, 896)
+        "}" ::"r"(o), "r"(pa), "l"(bv), "r"(idesc), "r"(acc)
+        : "memory");
+}
+#undef QTB_PV
+// S = Q K^T over HD/16 k-steps (K-major SW128 descriptors, as mma_ss2).  %0 d, %1 a, %2 b, %3 idesc
+#define QTB_S1(OFF, P) "add.u64 x, %1, " #OFF ";\n\tadd.u64 y, %2, " #OFF ";\n\t" QTB_SS("%0", "x", "y", "%3", P)
+template <int HD>
+__device__ __forceinline__ void mma_s1(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    if constexpr (HD == 64) {
+        asm volatile("{\n\t.reg .pred E, F, T;\n\t.reg .b64 x, y;\n\t"
+                     "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 F, %3, %3;\n\tsetp.eq.b32 T, %3, %3;\n\t"
+                     QTB_S1(0, "F") QTB_S1(2, "T") QTB_S1(4, "T") QTB_S1(6, "T")
+                     "}" ::"r"(d), "l"(a), "l"(b), "r"(idesc)
+                     : "memory");
+    } else {
+        asm volatile("{\n\t.reg .pred E, F, T;\n\t.reg .b64 x, y;\n\t"
+                     "elect.sync _|E, 0xffffffff;\n\tsetp.ne.b32 F, %3, %3;\n\tsetp.eq.b32 T, %3, %3;\n\t"
+                     QTB_S1(0, "F") QTB_S1(2, "T") QTB_S1(4, "T") QTB_S1(6, "T")
+                     QTB_S1(1024, "T") QTB_S1(1026, "T") QTB_S1(1028, "T") QTB_S1(1030, "T")
+                     "}" ::"r"(d), "l"(a), "l"(b), "r"(idesc)
+                     : "memory");
+    }
+}
+#undef QTB_S1
+
 template <int HD>
 struct BwdSmem {
     static constexpr int TILE = 128 * HD * 2;
@@ -1221,11 +1348,8 @@ __global__ void __launch_bounds__(NT, 1) dkdv_tc_kernel(const __grid_constant__ 
             if (t >= P::NB) mbar_wait(&b_free[buf], ((t - P::NB) / P::NB) & 1);
             tc_fence_after();
             const uint32_t qa = s_base + S::OFF_R + st * 2 * S::TILE + sub * 64 * 128, oa = qa + S::TILE;
-#pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) {
-                mma_bf16_ss(tmem + buf * 128, kdesc(ka, kk, 128 * 128), kdesc(qa, kk, 128 * 128), idesc_s, kk > 0);
-                mma_bf16_ss(tmem + buf * 128 + 64, kdesc(va, kk, 128 * 128), kdesc(oa, kk, 128 * 128), idesc_s, kk > 0);
-            }
+            mma_ss2<HD>(tmem + buf * 128, kdesc(ka, 0, 128 * 128), kdesc(qa, 0, 128 * 128), tmem + buf * 128 + 64,
+                        kdesc(va, 0, 128 * 128), kdesc(oa, 0, 128 * 128), idesc_s);
             tc_commit(&s_full[buf]);
         };
         issue_s(0);
@@ -1236,14 +1360,17 @@ __global__ void __launch_bounds__(NT, 1) dkdv_tc_kernel(const __grid_constant__ 
             tc_fence_after();
             const uint32_t qa = s_base + S::OFF_R + st * 2 * S::TILE, oa = qa + S::TILE;
             const uint32_t pb = tmem + buf * 128;
+            if (plo) {
+                mma_g4_hilo(tmem + P::ACC, tmem + P::ACC + HD, pb, mndesc(oa, 4 * sub, 128 * 128),
+                            mndesc(qa, 4 * sub, 128 * 128), idesc_g, t != 0);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t bo = mndesc(oa, kk + 4 * sub, 128 * 128), bq = mndesc(qa, kk + 4 * sub, 128 * 128);
-                const uint32_t acc = (t | kk) != 0;
-                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bo, idesc_g, acc);
-                if (plo) mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bo, idesc_g, 1);
-                mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 0), bq, idesc_g, acc);
-                if (plo) mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 1), bq, idesc_g, 1);
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t bo = mndesc(oa, kk + 4 * sub, 128 * 128), bq = mndesc(qa, kk + 4 * sub, 128 * 128);
+                    const uint32_t acc = (t | kk) != 0;
+                    mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bo, idesc_g, acc);
+                    mma_bf16_ts(tmem + P::ACC + HD, pb + 64 + a_col(kk, 0), bq, idesc_g, acc);
+                }
             }
             tc_commit(&b_free[buf]);
             if (sub == 1) tc_commit(&r_empty[st]);
@@ -1464,11 +1591,8 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
             tc_fence_after();
             const uint32_t qa = s_base + S::OFF_A + slot * S::TILE, oa = s_base + S::OFF_B + slot * S::TILE;
             const uint32_t ka = s_base + S::OFF_R + st * 2 * S::TILE + sub * 64 * 128, va = ka + S::TILE;
-#pragma unroll
-            for (int kk = 0; kk < HD / 16; ++kk) {
-                mma_bf16_ss(tmem + buf * 128, kdesc(qa, kk, 128 * 128), kdesc(ka, kk, 128 * 128), idesc_s, kk > 0);
-                mma_bf16_ss(tmem + buf * 128 + 64, kdesc(oa, kk, 128 * 128), kdesc(va, kk, 128 * 128), idesc_s, kk > 0);
-            }
+            mma_ss2<HD>(tmem + buf * 128, kdesc(qa, 0, 128 * 128), kdesc(ka, 0, 128 * 128), tmem + buf * 128 + 64,
+                        kdesc(oa, 0, 128 * 128), kdesc(va, 0, 128 * 128), idesc_s);
             tc_commit(&s_full[buf]);
             if (sub == 1 && j == per_head - 1) tc_commit(&qo_empty[slot]);  // last use of this head's Q/dO
         };
@@ -1482,11 +1606,13 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
             tc_fence_after();
             const uint32_t ka = s_base + S::OFF_R + st * 2 * S::TILE;
             const uint32_t pb = tmem + buf * 128;
+            if (plo) {
+                mma_dq4_hilo(tmem + P::ACC, pb, mndesc(ka, 4 * sub, 128 * 128), idesc_g, (j | sub) != 0);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t bk = mndesc(ka, kk + 4 * sub, 128 * 128);
-                mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), bk, idesc_g, (j | sub | kk) != 0);
-                if (plo) mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 1), bk, idesc_g, 1);
+                for (int kk = 0; kk < 4; ++kk)
+                    mma_bf16_ts(tmem + P::ACC, pb + a_col(kk, 0), mndesc(ka, kk + 4 * sub, 128 * 128), idesc_g,
+                                (j | sub | kk) != 0);
             }
             tc_commit(&b_free[buf]);
             if (sub == 1) {
@@ -1721,9 +1847,7 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
             auto s_mma = [&](int x) {
                 const uint32_t ka = s_base + S::OFF_K + ks * S::K;
                 const uint32_t qa_ = s_base + S::OFF_Q + x * S::Q;
-#pragma unroll
-                for (int kk = 0; kk < HD / 16; ++kk)
-                    mma_bf16_ss(tmem + x * 128, kdesc(qa_, kk, BQ * 128), kdesc(ka, kk, BKV * 128), idesc_s, kk > 0);
+                mma_s1<HD>(tmem + x * 128, kdesc(qa_, 0, BQ * 128), kdesc(ka, 0, BKV * 128), idesc_s);
                 tc_commit(&s_full[x]);
                 if (++s_issued == s_total) tc_commit(q_empty);  // Q no longer read by this item
             };
@@ -1750,11 +1874,12 @@ __global__ void __launch_bounds__(NT, 1) fwd2q_tc_kernel(const __grid_constant__
                     tc_fence_after();
                     const uint32_t pa = tmem + x * 128;
                     const uint32_t od = tmem + 256 + x * HD;
+                    if (plo) {
+                        mma_pv8_hilo(od, pa, mndesc(va, 0, BKV * 128), idesc_o, j != 0);
+                    } else {
 #pragma unroll
-                    for (int kk = 0; kk < BKV / 16; ++kk) {
-                        const uint64_t bd = mndesc(va, kk, BKV * 128);
-                        mma_bf16_ts(od, pa + a_col(kk, 0), bd, idesc_o, (j | kk) != 0);
-                        if (plo) mma_bf16_ts(od, pa + a_col(kk, 1), bd, idesc_o, 1);
+                        for (int kk = 0; kk < BKV / 16; ++kk)
+                            mma_bf16_ts(od, pa + a_col(kk, 0), mndesc(va, kk, BKV * 128), idesc_o, (j | kk) != 0);
                     }
                     tc_commit(&pv_done[x]);
                     ++pvcnt[x];
