@@ -1,7 +1,9 @@
 #!/bin/bash
-mkdir -p gpurun_out
-L=paper_2512_15306_b200/libqtrain_b200.so
-cp $L /tmp/new.so
-cp scratch/old.so $L; timeout 300 python scripts/attn_time.py > gpurun_out/attn_old.log 2>&1; echo "old"; tail -2 gpurun_out/attn_old.log
-cp /tmp/new.so $L; timeout 300 python scripts/attn_time.py > gpurun_out/attn_new.log 2>&1; echo "new"; tail -2 gpurun_out/attn_new.log
-timeout 600 python -m pytest tests/test_fused_gpu.py tests/test_bench_shapes_gpu.py -x -q -k "attention or attn" > gpurun_out/a1.log 2>&1; echo "attn rc=$?"; tail -3 gpurun_out/a1.log
+QTB_ATTN_NOWAIT=0 timeout 300 python scripts/attn_nowait.py
+QTB_ATTN_NOWAIT=1 timeout 300 python scripts/attn_nowait.py
+python - <<'PY'
+import torch, glob
+for f in sorted(glob.glob("/tmp/fwd_0_*.pt")):
+    a = torch.load(f); b = torch.load(f.replace("fwd_0_", "fwd_1_"))
+    print(f, "nowait vs wait bitwise:", all(torch.equal(x, y) for x, y in zip(a, b)))
+PY
