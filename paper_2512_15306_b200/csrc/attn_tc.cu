@@ -1629,10 +1629,20 @@ __global__ void __launch_bounds__(NT, 1) dq_tc_kernel(const __grid_constant__ CU
         const float c_s = inv_sqrt_d * LOG2E;
         const int64_t grow = (int64_t)b * T + q;
         int t = 0;
+        // the row's LSE / D of the next head are loaded one head ahead (their latency otherwise
+        // stalls every head switch)
+        float Ln = 0.0f, Dn = 0.0f;
+        if (qok) {
+            Ln = lse[((int64_t)b * H + hbase) * T + q];
+            Dn = Dv[((int64_t)b * H + hbase) * T + q];
+        }
         for (int hh = 0; hh < group; ++hh) {
             const int h = hbase + hh;
-            const float Lq = qok ? lse[((int64_t)b * H + h) * T + q] : 0.0f;
-            const float Dq = qok ? Dv[((int64_t)b * H + h) * T + q] : 0.0f;
+            const float Lq = Ln, Dq = Dn;
+            if (qok && hh + 1 < group) {
+                Ln = lse[((int64_t)b * H + h + 1) * T + q];
+                Dn = Dv[((int64_t)b * H + h + 1) * T + q];
+            }
             const float nl = -Lq * LOG2E, dsc = Dq * inv_sqrt_d;
             for (int js = 0; js < 2 * per_head; ++js, ++t) {
                 const int buf = t % P::NB;
