@@ -171,6 +171,8 @@ void qtk_attn_set_fwd2q(int on);
 /* RMSNorm path: 0 by shape, 1 split-role chain kernel on the streaming path, 2 split-role chain + row
  * kernels everywhere, 3 (default) forward as 2 and backward as 1; all bit-identical outputs */
 void qtk_rms_set_path(int mode);
+/* RoPE kernel: 1 (default) head-looped (table chunk loaded once per row), 0 per-item; bitwise equal */
+void qtk_rope_set_heads(int on);
 int qtk_attn_fwd(const void* qkv, int B, int T, int H, int Hkv, int hd, int qkv_dim, void* out, int64_t ldo,
                  float* out32, float* lse, uint32_t* amax, cudaStream_t s);
 /* precision mode (process-wide): fast_exp = __expf for exp(); bwd_split = P and

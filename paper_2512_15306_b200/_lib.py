@@ -61,6 +61,7 @@ _SIGS = {
     "qtk_attn_set_plo": (None, [C.c_int]),
     "qtk_attn_set_fwd2q": (None, [C.c_int]),
     "qtk_rms_set_path": (None, [C.c_int]),
+    "qtk_rope_set_heads": (None, [C.c_int]),
     "qtk_rope": (C.c_int, [c_vp, c_i64, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, C.c_int, c_vp, c_vp]),
     "qtk_gemm_plan": (C.c_int, [C.POINTER(QtkGemm)] + [C.POINTER(C.c_int)] * 5),
     "qtk_embed_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, c_vp, C.c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -310,3 +310,29 @@ def test_rmsnorm_split_role_chain_bitwise(ops, rows, d, resid):
             assert torch.equal(o[5], outs[0][5])
         else:  # fused partials (R rows) vs 16-row partials: same sums, regrouped
             torch.testing.assert_close(o[5], outs[0][5], rtol=2e-4, atol=1e-6)
+
+
+@pytest.mark.parametrize("rows,T,H,Hkv,hd", [(16384, 1024, 14, 2, 64), (8192, 1024, 32, 32, 128), (300, 100, 4, 1, 64)])
+def test_rope_head_looped_kernel_bitwise(rows, T, H, Hkv, hd):
+    """rope_heads_kernel (one table chunk per row, looped over the heads) equals the per-item
+    kernel bit for bit, forward and backward (with the whole-row absmax)."""
+    from paper_2512_15306_b200 import _lib
+    L = _lib.lib()
+    q = (H + 2 * Hkv) * hd
+    g = torch.Generator(device="cuda").manual_seed(rows + hd)
+    x = (torch.randn(rows, q, device="cuda", generator=g) * 2).to(torch.bfloat16)
+    tab = torch.randn(T, hd // 2, 2, device="cuda", generator=g)
+    try:
+        for bwd in (0, 1):
+            outs = []
+            for mode in (0, 1):
+                L.qtk_rope_set_heads(mode)
+                xt = x.clone()
+                am = torch.zeros(1, dtype=torch.int32, device="cuda")
+                rc = L.qtk_rope(xt.data_ptr(), rows, T, H + Hkv, hd, q, tab.data_ptr(), bwd,
+                                am.data_ptr() if bwd else None, torch.cuda.current_stream().cuda_stream)
+                assert rc == 0
+                outs.append((xt, am))
+            assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    finally:
+        L.qtk_rope_set_heads(1)
