@@ -73,6 +73,15 @@ int main(int argc, char** argv) {
     } catch (const std::runtime_error& e) {
         threw = std::strstr(e.what(), "adamw_step: non-finite gradient in") != nullptr;
     }
+    // a per-call recompute set other than the session's is rejected (invalid_argument)
+    bool rejected = false;
+    try {
+        const auto sc = qt::build_step_context(cfg, params, prec);
+        qt::model_forward(cfg, params, sc, toks, batch, qt::RecomputeSet::block(), prec);
+    } catch (const std::invalid_argument& e) {
+        rejected = std::strstr(e.what(), "recompute set differs") != nullptr;
+    }
+    threw = threw && rejected;
     std::printf("%s first %.5f last %.5f checkpoint %s errors %s\n", last < first && same && threw ? "OK" : "FAIL",
                 first, last, same ? "bitwise" : "DIFFERS", threw ? "ok" : "WRONG");
     return last < first && same && threw ? 0 : 1;

@@ -214,19 +214,27 @@ struct ForwardResult {  // model.hpp:163-175 (the loss; activations stay on the 
     float loss = 0.0f;
 };
 
+// The recompute set sizes the session's saved-activation buffers, so it is fixed when the
+// session is created (RunPlan::recompute); a call asking for another set is rejected rather
+// than silently run with the session's.  ChunkSpec only changes the reference's working-set
+// layout (results are identical), so it is accepted and ignored.
 inline ForwardResult model_forward(const ModelConfig&, Session& params, const StepContext& step,
                                    const std::vector<std::int32_t>& tokens, std::int64_t batch,
-                                   const RecomputeSet& /*recompute*/, const PrecisionMap&, const ChunkSpec& = {},
+                                   const RecomputeSet& recompute, const PrecisionMap&, const ChunkSpec& = {},
                                    bool with_grads = true) {
     if (step.session != &params) throw std::invalid_argument("model_forward: step context of another model");
+    if (recompute.bits != params.recompute().bits)
+        throw std::invalid_argument("model_forward: recompute set differs from the session's (RunPlan::recompute)");
     return ForwardResult{params.model_forward(tokens, batch, with_grads)};
 }
 
 // model_backward + GradAccumulator::accumulate (model.hpp:190-211): gradients are
 // accumulated into the session's GradAccumulator at micro_step
 inline void model_backward(const ModelConfig&, Session& params, const StepContext&, ForwardResult&,
-                           const RecomputeSet&, const PrecisionMap&, const ChunkSpec& = {},
+                           const RecomputeSet& recompute, const PrecisionMap&, const ChunkSpec& = {},
                            std::uint64_t micro_step = 0) {
+    if (recompute.bits != params.recompute().bits)
+        throw std::invalid_argument("model_backward: recompute set differs from the session's (RunPlan::recompute)");
     params.model_backward(micro_step);
 }
 
