@@ -1,5 +1,5 @@
 #!/bin/bash
-L=paper_2512_15306_b200/libqtrain_b200.so
-timeout 900 python -m pytest tests/test_fused_gpu.py tests/test_parity_more_gpu.py -x -q -k "rms or norm" 2>&1 | tail -2
-RMS_M=8192 RMS_D=4096 timeout 300 python scripts/rms_ab.py $L 2>&1 | grep rms_ | sed 's/^/7b /'
-RMS_M=4096 RMS_D=5120 timeout 300 python scripts/rms_ab.py $L 2>&1 | grep rms_ | sed 's/^/14b /'
+mkdir -p gpurun_out/fin
+timeout 2400 python -m pytest tests/ -q -m gpu --timeout=900 > gpurun_out/fin/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/fin/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/fin/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/fin/smoke.log
+timeout 900 python bench.py > gpurun_out/fin/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/fin/bench.log | cut -c1-200
