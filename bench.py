@@ -25,6 +25,8 @@ import time
 ROOT = pathlib.Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
+TOKENS_PER_OPT_STEP = 500_000
+
 # B200 dense spec peaks used by the reference's MFU formula (src/memplan.cpp:307-312)
 P_FP8_SPEC = 4.5e15
 P_BF16_SPEC = 2.25e15
@@ -208,8 +210,8 @@ def run_reference_arm(args, cfg, B, T, world):
         "impl": "reference", "metric": "fp8_train_tokens_per_sec", "value": value, "unit": "tokens/s",
         "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp8(e4m3 fwd / e5m2 grads) emulated on CPU", "data": "synthetic",
-        "config": {"workload": args.config, "model": args.config, "global_batch": B * max(world, 1), "seq_len": T,
-                   "parallelism": "cpu processes"},
+        "config": {"workload": args.config, "model": args.config, "global_batch": args.grad_accum * B * max(world, 1),
+                   "micro_batch": B, "grad_accum": args.grad_accum, "seq_len": T, "parallelism": "cpu processes"},
         "mfu": value * (fp8_f / P_FP8_SPEC + bf16_f / P_BF16_SPEC),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "reference",
                          "sample": _sample_text(cfg, sample_tokens, model) + f"; each step = {cores} independent "
@@ -230,6 +232,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="qwen2.5-0.5b")
     ap.add_argument("--micro-batch", type=int, default=0)
+    ap.add_argument("--grad-accum", type=int, default=0,
+                    help="micro-batches per optimizer step (RunPlan::ga_steps); a step = one optimizer step. "
+                         "0 = the paper's protocol: ~500k tokens per optimizer step per GPU (PAPER.md:366)")
     ap.add_argument("--seq", type=int, default=0)
     ap.add_argument("--grads", default="e5m2", choices=["e4m3", "e5m2"])
     ap.add_argument("--recompute", default="")
@@ -251,6 +256,11 @@ def main():
     B = args.micro_batch or default_mb.get(args.config, 8)
     T = args.seq or cfg.seq_len
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.grad_accum <= 0:
+        # the reference's throughput table is measured at a 500k-token optimizer batch
+        # ("trained at a per-step batch size of 500k"); per GPU, so the
+        # per-rank work stays fixed as N grows (weak scaling)
+        args.grad_accum = max(1, round(TOKENS_PER_OPT_STEP / (B * T)))
     if args.impl == "reference":
         run_reference_arm(args, cfg, B, T, world)
         return
@@ -268,7 +278,8 @@ def main():
         obj = [S.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
-    plan = S.RunPlan(micro_batch=B, ga_steps=1, recompute=tuple(x for x in args.recompute.split(",") if x),
+    GA = max(1, args.grad_accum)
+    plan = S.RunPlan(micro_batch=B, ga_steps=GA, recompute=tuple(x for x in args.recompute.split(",") if x),
                      moments=args.moments, shard_grads=args.shard_grads, shard_weights=args.shard_weights,
                      offload=tuple(x for x in args.offload.split(",") if x), transfer_policy=args.transfer_policy)
     sess = S.Session(cfg, S.PrecisionMap(backward_grads=args.grads), plan, S.AdamWHyper(), seed=1234, rank=rank,
@@ -279,7 +290,7 @@ def main():
     # synthetic uniform token ids (tests/test_model.cpp:29-35 layout: B*(T+1) per micro-batch)
     nbatches = 4
     g = np.random.default_rng(1000 + rank)
-    host = [g.integers(0, cfg.vocab, size=B * (T + 1), dtype=np.int32) for _ in range(nbatches)]
+    host = [g.integers(0, cfg.vocab, size=GA * B * (T + 1), dtype=np.int32) for _ in range(nbatches)]
     dev = [torch.from_numpy(h).cuda() for h in host]
     pinned = [torch.from_numpy(h).pin_memory() for h in host]
 
@@ -313,7 +324,7 @@ def main():
         ms = t.item()
 
     # ---- end to end through the public API: pinned host tokens H2D + loss D2H every step
-    h2d = B * (T + 1) * 4
+    h2d = GA * B * (T + 1) * 4
     d2h = 4 + 4
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -337,7 +348,7 @@ def main():
     prof = sess.profile()
     sess.set_profile(False)
 
-    tokens_per_step = B * T * world
+    tokens_per_step = GA * B * T * world
     value = tokens_per_step / (ms / 1e3)
     e2e_value = tokens_per_step / (ms_e2e / 1e3)
     fp8_f, bf16_f = cfg.flops_per_token()
@@ -373,7 +384,7 @@ def main():
                 "frac": achieved / peaks["hbm_gbs"], "peak_basis": f"measured copy [{peaks['src']}]",
                 "launches": dom["launches"], "share_of_step": dom["ms"] / total_ms, "traffic": None}
     if dom_name == "gemm_fp8":
-        roof["algorithmic_bytes_per_launch"] = fp8_gemm_bytes_per_step(cfg, B * T) / max(dom["launches"], 1)
+        roof["algorithmic_bytes_per_launch"] = GA * fp8_gemm_bytes_per_step(cfg, B * T) / max(dom["launches"], 1)
     # DRAM bytes per launch of the dominant class from the committed ncu capture of one step
     # (scripts/traffic_summary.py; cold-cache serialised replay), when it matches this config
     tf = next((ROOT / "profiles" / f"r{r:02d}_traffic_0.5b.json" for r in (2, 1)
@@ -397,8 +408,8 @@ def main():
         "metric": "fp8_train_tokens_per_sec", "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "fp8", "data": "synthetic",
-        "config": {"workload": args.config, "model": args.config, "global_batch": B * world, "micro_batch": B,
-                   "seq_len": T, "parallelism": f"dp{world}" + ("+zero1" if world > 1 else ""),
+        "config": {"workload": args.config, "model": args.config, "global_batch": GA * B * world, "micro_batch": B,
+                   "grad_accum": GA, "tokens_per_step": GA * B * T * world, "seq_len": T, "parallelism": f"dp{world}" + ("+zero1" if world > 1 else ""),
                    "grads": args.grads, "recompute": args.recompute or "none", "moments": args.moments,
                    "shard_grads": args.shard_grads, "shard_weights": args.shard_weights,
                    "offload": args.offload or "none", "transfer_policy": args.transfer_policy,
