@@ -393,7 +393,8 @@ def main():
         try:
             t = json.loads(tf.read_text())["classes"].get(dom_name)
             if t:
-                per_call = t["dram_bytes_per_launch"] * t["launches"] / max(dom["launches"], 1)
+                # the capture is one GA = 1 step; the profiled step here has GA micro-steps
+                per_call = t["dram_bytes_per_launch"] * t["launches"] * GA / max(dom["launches"], 1)
                 roof["traffic"] = per_call
                 roof["traffic_unit"] = "bytes/launch (dram read+write, ncu)"
                 roof["traffic_source"] = str(tf.relative_to(ROOT))

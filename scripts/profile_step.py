@@ -19,13 +19,14 @@ ap.add_argument("--config", default="qwen2.5-0.5b")
 ap.add_argument("--micro-batch", type=int, default=16)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--recompute", default="")
+ap.add_argument("--ga", type=int, default=1, help="micro-batches per step (the bench default accumulates ~500k tokens)")
 args = ap.parse_args()
 cfg = S.PRESETS[args.config]
 B, T = args.micro_batch, cfg.seq_len
-plan = S.RunPlan(micro_batch=B, ga_steps=1, recompute=tuple(x for x in args.recompute.split(",") if x))
+plan = S.RunPlan(micro_batch=B, ga_steps=args.ga, recompute=tuple(x for x in args.recompute.split(",") if x))
 sess = S.Session(cfg, S.PrecisionMap(backward_grads="e5m2"), plan, S.AdamWHyper(), seed=1234)
 sess.init_params(1234)
-tok = torch.from_numpy(np.random.default_rng(0).integers(0, cfg.vocab, size=B * (T + 1), dtype=np.int32)).cuda()
+tok = torch.from_numpy(np.random.default_rng(0).integers(0, cfg.vocab, size=args.ga * B * (T + 1), dtype=np.int32)).cuda()
 for i in range(args.warmup):
     sess.train_step(tok, B, step=i, sync=False)
 sess.sync()
