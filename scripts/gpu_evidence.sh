@@ -11,7 +11,7 @@ if [ -z "${SKIP_BENCH:-}" ]; then
 timeout 900 python bench.py > gpurun_out/ev/bench_0.5b.log 2>&1; echo "bench rc=$?"
 timeout 900 python bench.py --grad-accum 1 --no-cpu-baseline > gpurun_out/ev/bench_0.5b_ga1.log 2>&1; echo "bench ga1 rc=$?"
 timeout 900 python bench.py --impl reference > gpurun_out/ev/bench_reference.log 2>&1; echo "ref rc=$?"
-timeout 900 python bench.py --config llama-7b --micro-batch 8 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_7b.log 2>&1; echo "7b rc=$?"
+timeout 900 python bench.py --config llama-7b --micro-batch 12 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_7b.log 2>&1; echo "7b rc=$?"
 timeout 900 python bench.py --config llama-7b --micro-batch 8 --grad-accum 1 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_7b_ga1.log 2>&1; echo "7b ga1 rc=$?"
 timeout 900 python bench.py --config qwen2.5-1.5b --micro-batch 8 --recompute block --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_15b.log 2>&1; echo "1.5b rc=$?"
 timeout 1500 python bench.py --config qwen2.5-14b --micro-batch 4 --grad-accum 16 --moments bf16_sr --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/ev/bench_14b.log 2>&1; echo "14b rc=$?"
