@@ -60,7 +60,8 @@ struct alignas(64) Params {
     const uint16_t* res;
     int64_t ldr;
     uint64_t sr_seed, sr_stream, sr_base;
-    const uint64_t* sr_ms;  // device micro-step: base = *sr_ms * M * N (graph replay), else sr_base
+    const uint64_t* sr_ms;  // device micro-step: base = *sr_ms * sr_mn + sr_off (graph replay), else sr_base
+    uint64_t sr_mn, sr_off;  // full GEMM's M*N and this launch's first-row counter offset (tail split)
 };
 
 // CG = CTAs per MMA (tcgen05 cta_group): 2 pairs two SMs on a 256-row tile
@@ -175,7 +176,7 @@ __device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col
         }
     } else {  // *_ACC: GradAccumulator::accumulate fused (src/model.cpp:455-462)
         uint16_t* buf = reinterpret_cast<uint16_t*>(p.out) + (int64_t)row * p.ldo + col0;
-        const uint64_t sb = p.sr_ms ? *p.sr_ms * (uint64_t)p.M * (uint64_t)p.N : p.sr_base;
+        const uint64_t sb = p.sr_ms ? *p.sr_ms * p.sr_mn + p.sr_off : p.sr_base;
         const uint64_t ctr0 = sb + (uint64_t)row * (uint64_t)p.N + (uint64_t)col0;
         const uint64_t key = rng_key(p.sr_seed, p.sr_stream);
         if (vec) {
@@ -227,7 +228,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const Params& p, uint32_t tmem
     const int row = m_row0 + lane;
     const uint64_t key = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) ? rng_key(p.sr_seed, p.sr_stream) : 0;
     const uint64_t sr_base = (EPI == EPI_BF16_ACC || EPI == EPI_F32_ACC) && p.sr_ms
-                                 ? *p.sr_ms * (uint64_t)p.M * (uint64_t)p.N
+                                 ? *p.sr_ms * p.sr_mn + p.sr_off
                                  : p.sr_base;
     constexpr bool SWI = EPI == EPI_SWIGLU_BWD;
     if constexpr (LOADS && !SWI) {
@@ -633,8 +634,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int S, int M,
                                      const float* __restrict__ a_scale, const float* __restrict__ b_scale,
                                      void* __restrict__ out, int64_t ldo, const uint16_t* __restrict__ res,
                                      int64_t ldr, uint64_t seed, uint64_t stream, uint64_t base,
-                                     const uint64_t* ms) {
-    if (ms) base = *ms * (uint64_t)M * (uint64_t)N;
+                                     const uint64_t* ms, uint64_t ms_mn, uint64_t ms_off) {
+    if (ms) base = *ms * ms_mn + ms_off;
     float denom = 1.0f;
     if (a_scale && b_scale) denom = __fmul_rn(*a_scale, *b_scale);
     const float rcp = __frcp_rn(denom);
@@ -851,6 +852,43 @@ int choose_splits(int64_t M, int64_t N, int64_t K, int kind, int bn, int cg) {
     return (int)std::max<int64_t>(s, 1);
 }
 
+// Tail split: when the persistent tile loop's last round is at most half full and K is
+// long, the GEMM runs as a head of whole M panels filling the earlier rounds exactly plus
+// a split-K tail over the remaining panels (the idle CTAs of the last round share its K
+// loop).  0.5B gate_up wgrad (M 9728, N 896, K 16384): 152 pair tiles on 74 pairs = 2.05
+// rounds -> 148 tiles + 4 tiles split 16 ways.  ws_bytes < 0: no workspace bound (sizing).
+bool tail_plan(int64_t M, int64_t N, int64_t K, int kind, int cg, int bn, int64_t ws_bytes, int64_t* m_head,
+               int* s_tail) {
+    const int slots = num_sms() / cg;
+    const int64_t bmc = (int64_t)BM * cg;
+    const int64_t num_m = ceil_div(M, bmc), num_n = ceil_div(N, (int64_t)bn), tiles = num_m * num_n;
+    const int64_t rounds = ceil_div(tiles, (int64_t)slots);
+    if (rounds < 2 || N % 4) return false;
+    if ((tiles - (rounds - 1) * slots) * 2 > slots) return false;
+    // the head + split tail + reduce cost two extra launch ramps (~15 us): only worth it for
+    // long K split many ways (measured: gate_up wgrad 130 -> 120 us at K = 16384, S = 16; the
+    // down forward / gate_up dgrad at K = 4864 / 9728, S = 2 got slower, scripts/gemm_tail.py)
+    const int64_t nk = ceil_div(K, (int64_t)(kind == 0 ? 128 : 64));
+    if (nk < 64) return false;
+    const int64_t hp = (rounds - 1) * slots / num_n;  // head M panels
+    if (hp < 1 || hp >= num_m) return false;
+    const int64_t mt = M - hp * bmc, tt = (num_m - hp) * num_n;
+    int64_t sp = std::min<int64_t>(std::min<int64_t>(slots / tt, nk / 4), 16);
+    while (ws_bytes >= 0 && sp >= 4 && sp * mt * N * 4 > ws_bytes) --sp;
+    if (sp < 4) return false;
+    *m_head = hp * bmc;
+    *s_tail = (int)sp;
+    return true;
+}
+bool tail_split_enabled() {
+    static int f = -1;
+    if (f < 0) {
+        const char* e = getenv("QTB_GEMM_TAIL");
+        f = e ? atoi(e) : 1;
+    }
+    return f != 0;
+}
+
 }  // namespace gemm
 }  // namespace qtb
 
@@ -863,6 +901,10 @@ extern "C" int qtk_gemm_splitk_ws_bytes(int64_t M, int64_t N, int64_t K, int kin
         const int bn = (tc.cg == 2 && kind == 0 && bmn && tc.bn == 128) ? 256 : tc.bn;
         const int s = qtb::gemm::choose_splits(M, N, K, kind, bn, tc.cg);
         if (s > 1) best = std::max(best, (int)std::min<int64_t>((int64_t)s * M * N * 4, INT32_MAX));
+        int64_t mh = 0;
+        int st = 0;
+        if (s <= 1 && qtb::gemm::tail_split_enabled() && qtb::gemm::tail_plan(M, N, K, kind, tc.cg, bn, -1, &mh, &st))
+            best = std::max(best, (int)std::min<int64_t>((int64_t)st * (M - mh) * N * 4, INT32_MAX));
     }
     return best;
 }
@@ -874,8 +916,9 @@ namespace gemm {
 struct Decision {
     int cg, bn, splits;
 };
-Decision decide(const QtkGemm* g) {
-    const TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0, g->K);
+Decision decide(const QtkGemm* g, int force_cg = 0) {
+    TileCfg tc = choose_cfg(g->M, g->N, g->kind, g->b_mn != 0, g->K);
+    if (force_cg) tc.cg = force_cg;  // tail-split head: the full GEMM's tile shape
     Decision d{tc.cg, (g->bn == 128 || g->bn == 256) ? g->bn : tc.bn, 1};
     const bool ce = g->ce_stats != nullptr;
     if (ce) d.bn = 256;  // one 128-column statistics block per epilogue warp half
@@ -914,7 +957,10 @@ extern "C" int qtk_gemm_plan(const QtkGemm* g, int* cg, int* bn, int* splits, in
     return 0;
 }
 
-extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
+// One launch (or split-K launch + reduce) of *g.  sr_row0 = global row of g's first row
+// and M_full = the full GEMM's M when g is a tail-split part (the SR counters stay those of
+// the unsplit GEMM); force_cg = the full GEMM's cta_group for the head part.
+static int gemm_run(const QtkGemm* g, cudaStream_t s, int64_t sr_row0, int64_t M_full, int force_cg) {
     using namespace qtb::gemm;
     if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;
     const int elem = g->kind == 0 ? 1 : 2;
@@ -924,7 +970,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
         ((g->lda * elem) & 15) || ((g->ldb * elem) & 15))
         return 1;
     if (g->lda < (g->a_mn ? g->M : g->K) || g->ldb < (g->b_mn ? g->N : g->K)) return 1;
-    const Decision dec = decide(g);
+    const Decision dec = decide(g, force_cg);
     const int cg = dec.cg;
     const int bn = dec.bn;
     const bool ce = g->ce_stats != nullptr;
@@ -969,8 +1015,11 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     p.ldr = g->ldr;
     p.sr_seed = g->sr_seed;
     p.sr_stream = g->sr_stream;
-    p.sr_base = g->sr_base;
+    const uint64_t sr_off = (uint64_t)sr_row0 * (uint64_t)g->N;
+    p.sr_base = g->sr_base + sr_off;
     p.sr_ms = g->sr_micro_step;
+    p.sr_mn = (uint64_t)M_full * (uint64_t)g->N;
+    p.sr_off = sr_off;
     const int tiles = p.num_m * p.num_n;
     const int splits = dec.splits;
     p.splits = splits;
@@ -994,7 +1043,7 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
                                                 FastDiv((uint32_t)(g->N / 4)), g->epi,
                                                 g->a_scale, g->b_scale, g->out, g->ldo,
                                                 reinterpret_cast<const uint16_t*>(g->res), g->ldr, g->sr_seed,
-                                                g->sr_stream, g->sr_base, g->sr_micro_step);
+                                                g->sr_stream, g->sr_base + sr_off, g->sr_micro_step, p.sr_mn, sr_off);
         return (int)cudaGetLastError();
     }
     // staged TMA-store epilogue: 16-B aligned output (and residual) rows
@@ -1035,4 +1084,32 @@ extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     }
     const int grid = std::min(tiles, num_sms() / cg) * cg;
     return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, cg, s);
+}
+
+extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
+    using namespace qtb::gemm;
+    if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;
+    const Decision d = decide(g);
+    int64_t m_head = 0;
+    int s_tail = 0;
+    if (tail_split_enabled() && d.splits == 1 && g->ws && g->split_k == 0 && !g->ce_stats && !g->a2 &&
+        g->epi != EPI_SWIGLU_BWD && g->ldo % 4 == 0 &&
+        tail_plan(g->M, g->N, g->K, g->kind, d.cg, d.bn, g->ws_bytes, &m_head, &s_tail)) {
+        const int elem = g->kind == 0 ? 1 : 2;
+        const int oel = g->epi == EPI_F32 ? 4 : 2;
+        QtkGemm h = *g;
+        h.M = m_head;
+        h.split_k = 1;
+        h.bn = d.bn;
+        int rc = gemm_run(&h, s, 0, g->M, d.cg);
+        if (rc) return rc;
+        QtkGemm t = *g;
+        t.M = g->M - m_head;
+        t.split_k = s_tail;
+        t.a = static_cast<const uint8_t*>(g->a) + (g->a_mn ? m_head : m_head * g->lda) * elem;
+        t.out = static_cast<uint8_t*>(g->out) + m_head * g->ldo * oel;
+        if (g->res) t.res = static_cast<const uint8_t*>(g->res) + m_head * g->ldr * 2;
+        return gemm_run(&t, s, m_head, g->M, 0);
+    }
+    return gemm_run(g, s, 0, g->M, 0);
 }
