@@ -343,6 +343,9 @@ int qt_rope_table(int T, int hd, float* host_out);
 /* which instantiation qtk_gemm launches for *g (no launch): cta_group, BN,
  * split-K factor, grid, output tiles per CTA of the persistent loop */
 int qtk_gemm_plan(const QtkGemm* g, int* cg, int* bn, int* splits, int* grid, int* tiles_per_cta);
+/* whether qtk_gemm runs *g as a tail split (head launch of *m_head rows + a split-K launch
+ * of the remaining rows split *s_tail ways): 1 yes, 0 no (then *m_head = M, *s_tail = 1) */
+int qtk_gemm_tail_plan(const QtkGemm* g, int64_t* m_head, int* s_tail);
 int qt_count_step_kernels(qt_session* s, const int32_t* tokens_dev, int64_t tokens_per_mb, int64_t batch,
                           int64_t* kernels, int64_t* other_nodes);
 /* diagnostic: one trainer step captured into a CUDA graph and replayed `iters` times

@@ -64,6 +64,7 @@ _SIGS = {
     "qtk_rope_set_heads": (None, [C.c_int]),
     "qtk_rope": (C.c_int, [c_vp, c_i64, C.c_int, C.c_int, C.c_int, C.c_int, c_vp, C.c_int, c_vp, c_vp]),
     "qtk_gemm_plan": (C.c_int, [C.POINTER(QtkGemm)] + [C.POINTER(C.c_int)] * 5),
+    "qtk_gemm_tail_plan": (C.c_int, [C.POINTER(QtkGemm), C.POINTER(c_i64), C.POINTER(C.c_int)]),
     "qtk_embed_fwd": (C.c_int, [c_vp, C.c_int, C.c_int, c_vp, C.c_int, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "qtk_embed_sort_scratch_bytes": (C.c_size_t, [C.c_int, c_i64]),
     "qtk_embed_sort": (C.c_int, [c_vp, C.c_int, c_i64, c_vp, C.c_size_t, c_vp, c_vp, c_vp, c_vp, c_vp]),

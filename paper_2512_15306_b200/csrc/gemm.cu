@@ -1086,15 +1086,27 @@ static int gemm_run(const QtkGemm* g, cudaStream_t s, int64_t sr_row0, int64_t M
     return dispatch(g->kind, g->a_mn != 0, g->b_mn != 0, bn, g->epi, p, grid, cg, s);
 }
 
+static bool use_tail(const QtkGemm* g, const qtb::gemm::Decision& d, int64_t* m_head, int* s_tail) {
+    using namespace qtb::gemm;
+    return tail_split_enabled() && d.splits == 1 && g->ws && g->split_k == 0 && !g->ce_stats && !g->a2 &&
+           g->epi != EPI_SWIGLU_BWD && g->ldo % 4 == 0 &&
+           tail_plan(g->M, g->N, g->K, g->kind, d.cg, d.bn, g->ws_bytes, m_head, s_tail);
+}
+
+extern "C" int qtk_gemm_tail_plan(const QtkGemm* g, int64_t* m_head, int* s_tail) {
+    *m_head = g->M;
+    *s_tail = 1;
+    if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;
+    return use_tail(g, qtb::gemm::decide(g), m_head, s_tail) ? 1 : 0;
+}
+
 extern "C" int qtk_gemm(const QtkGemm* g, cudaStream_t s) {
     using namespace qtb::gemm;
     if (g->M <= 0 || g->N <= 0 || g->K <= 0) return 0;
     const Decision d = decide(g);
     int64_t m_head = 0;
     int s_tail = 0;
-    if (tail_split_enabled() && d.splits == 1 && g->ws && g->split_k == 0 && !g->ce_stats && !g->a2 &&
-        g->epi != EPI_SWIGLU_BWD && g->ldo % 4 == 0 &&
-        tail_plan(g->M, g->N, g->K, g->kind, d.cg, d.bn, g->ws_bytes, &m_head, &s_tail)) {
+    if (use_tail(g, d, &m_head, &s_tail)) {
         const int elem = g->kind == 0 ? 1 : 2;
         const int oel = g->epi == EPI_F32 ? 4 : 2;
         QtkGemm h = *g;

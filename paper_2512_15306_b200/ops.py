@@ -93,6 +93,15 @@ def gemm_plan(a: torch.Tensor, b: torch.Tensor, **kw) -> dict:
     return dict(zip(("cg", "bn", "splits", "grid", "tiles_per_cta"), (x.value for x in o)))
 
 
+def gemm_tail_plan(a: torch.Tensor, b: torch.Tensor, **kw) -> tuple[int, int]:
+    """(head rows, tail split-K factor) when qtk_gemm runs the same arguments as a
+    tail split (head launch + split-K tail), else (M, 1)."""
+    g, _, _ = _gemm_desc(a, b, **kw)
+    mh, st = C.c_int64(), C.c_int()
+    on = _lib.lib().qtk_gemm_tail_plan(C.byref(g), C.byref(mh), C.byref(st))
+    return (mh.value, st.value) if on else (kw["M"], 1)
+
+
 def _gemm_desc(a, b, *, M, N, K, a_mn=False, b_mn=False, a_fmt=E4M3, b_fmt=E4M3, a_scale=None, b_scale=None,
                epi=EPI_BF16, out=None, res=None, sr=(0, 0, 0), bn=0, a2=None, split_k=1, amax=None, ce=None):
     _need_cuda(a, b)

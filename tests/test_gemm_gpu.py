@@ -216,3 +216,35 @@ def test_fp8_gemm_swiglu_backward_epilogue(ops, M, H, K):
     torch.cuda.synchronize()
     assert torch.equal(got.view(torch.int16), want.view(torch.int16))
     assert amax.item() == slot.item()
+
+
+@pytest.mark.parametrize("acc", [False, True])
+def test_gemm_tail_split_matches_single_launch(ops, acc):
+    """qtk_gemm's tail split (gemm.cu tail_plan) at the 0.5B gate_up wgrad shape
+    (M 9728 x N 896 x K 16384, both operands MN-major, E5M2 x E4M3): 152 pair tiles on
+    74 pairs run as a 148-tile head launch + the last M panel split-K 16 ways + the
+    deterministic reduce.  Against the single launch (itself checked against the
+    reference in test_bench_shapes_gpu.py): <= 1 bf16 ulp everywhere, >= 99.9 % bit-equal
+    (only the f32 summation order of the tail rows differs); the SR-accumulate epilogue
+    keeps the unsplit GEMM's counters, so the accumulate variant agrees the same way."""
+    T, F, d = 16384, 9728, 896
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randint(0, 120, (T, F), dtype=torch.uint8, device="cuda", generator=g)
+    b = torch.randint(0, 120, (T, d), dtype=torch.uint8, device="cuda", generator=g)
+    sa = torch.tensor([3.0], device="cuda")
+    sb = torch.tensor([5.0], device="cuda")
+    kw = dict(M=F, N=d, K=T, a_mn=True, b_mn=True, a_fmt=1, a_scale=sa, b_scale=sb)
+    acc0 = (torch.randn(F, d, device="cuda", generator=g) * 1e-2).to(torch.bfloat16)
+    if acc:
+        kw.update(epi=ops.EPI_BF16_ACC, sr=(7, 11, 123456))
+    mh, st = ops.gemm_tail_plan(a, b, split_k=0, **kw)
+    assert (mh, st) == (37 * 256, 16), (mh, st)
+    assert ops.gemm_tail_plan(a, b, split_k=1, **kw) == (F, 1)
+    outs = []
+    for sk in (1, 0):
+        o = acc0.clone() if acc else None
+        outs.append(ops.gemm(a, b, split_k=sk, out=o, **kw).float().cpu().numpy())
+    du = _ulp_diff(outs[0], outs[1])
+    assert du.max() <= 1, du.max()
+    assert (du == 0).mean() >= 0.999, (du == 0).mean()
+    assert (du[:mh] == 0).all()  # the head rows are the same launch shape: bit-identical
