@@ -26,7 +26,7 @@ python scripts/traffic_summary.py gpurun_out/ev/traffic_0.5b.csv gpurun_out/ev/t
 rm -f gpurun_out/ev/traffic_0.5b.csv
 fi
 if [ -z "${SKIP_FULL:-}" ]; then
-TAG=${TAG}final KERNELS="adamw_kernel ce_softmax_stats_kernel fwd2q_tc_kernel swiglu_bwd_kernel swiglu_fwd_kernel rms_chain2_kernel rms_bwd_fused_kernel rms_fwd_rows_kernel quantize_bf16_kernel dq_tc_kernel dkdv_tc_kernel rope_kernel" bash scripts/ncu_step.sh
+TAG=${TAG}final KERNELS="adamw_kernel ce_softmax_stats_kernel fwd2q_tc_kernel swiglu_bwd_kernel swiglu_fwd_kernel rms_chain2_kernel rms_bwd_rows_kernel rms_fwd_rows_kernel quantize_bf16_kernel dq_tc_kernel dkdv_tc_kernel rope_kernel" bash scripts/ncu_step.sh
 python scripts/ncu_summary.py gpurun_out/ncu/${TAG}final_*.raw.csv > gpurun_out/ncu/${TAG}final_ncu_summary.txt 2>&1
 fi
 for f in bench_0.5b bench_0.5b_ga1 bench_reference bench_7b bench_7b_ga1 bench_15b bench_14b; do tail -1 gpurun_out/ev/$f.log 2>/dev/null | cut -c1-300; done
